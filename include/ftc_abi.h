@@ -1,0 +1,214 @@
+/*
+ * ftc_abi.h -- C ABI of the B200-native ABFT-protected convolution
+ * (FT-CNN, arXiv 2003.12203).  Implemented by paper_2003_12203_b200/libftconv_b200.so.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference is a
+ * header-only C++20 library (proj/core/include/ftconv/); its API works on host
+ * Tensor4<T> objects and throws C++ exceptions.  Each entry point below replaces
+ * one reference interface (cited file:line, relative to proj/core/include/ftconv/)
+ * with plain pointers/sizes and a status code.  The C++ host API in
+ * include/ftconv_b200/ftconv.hpp restores the reference's names, Tensor4 values
+ * and exception semantics on top of this ABI.
+ *
+ * Memory: unless a function name ends in `_host`, every tensor pointer is a
+ * DEVICE pointer owned by the caller.  Tensors are dense NCHW, last dimension
+ * fastest (tensor.hpp:17-33): D is N x C x H x H, W is M x (C/groups) x R x R,
+ * O is N x M x E x E with E = (H + 2*pad - R)/stride + 1 (tensor.hpp:100-107).
+ * Checksums/summations are FP64 (the reference workflow at T=double).
+ *
+ * Streams: `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ * One protected layer may be in flight per layer handle.
+ *
+ * Errors: status codes map 1:1 to the reference exceptions (errors.hpp:9-27);
+ * ftc_last_error() returns the message of the calling thread's last failure.
+ */
+#ifndef FTC_ABI_H
+#define FTC_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTC_ABI_VERSION 1
+#define FTC_MAX_BLOCKS 4096
+#define FTC_MAX_STAGES 8
+
+/* errors.hpp:9-27 */
+typedef enum ftc_status {
+  FTC_OK = 0,
+  FTC_SHAPE_ERROR = 1,     /* ShapeError */
+  FTC_CONFIG_ERROR = 2,    /* ConfigError */
+  FTC_IO_ERROR = 3,        /* IoError */
+  FTC_INTEGRITY_ERROR = 4, /* IntegrityError: recompute failed twice (workflow.hpp:338) */
+  FTC_CUDA_ERROR = 5,      /* device/runtime failure (no reference counterpart) */
+  FTC_INVALID_ARGUMENT = 6
+} ftc_status;
+
+/* CkSel, checksums.hpp:14-23 */
+enum {
+  FTC_CK_O1 = 1u << 0, FTC_CK_O2 = 1u << 1, FTC_CK_O3 = 1u << 2, FTC_CK_O4 = 1u << 3,
+  FTC_CK_O5 = 1u << 4, FTC_CK_O6 = 1u << 5, FTC_CK_O7 = 1u << 6, FTC_CK_ALL = 0x7f
+};
+
+/* ResolveStage, report.hpp:12-21 */
+typedef enum ftc_stage {
+  FTC_STAGE_NONE = 0, FTC_STAGE_RELOAD, FTC_STAGE_COC, FTC_STAGE_RC, FTC_STAGE_CLC,
+  FTC_STAGE_FC, FTC_STAGE_DISCARD, FTC_STAGE_RECOMPUTE
+} ftc_stage;
+
+/* Layer geometry: Tensor4 shapes + ConvParams (tensor.hpp:92-97). */
+typedef struct ftc_conv_desc {
+  int32_t N;      /* batch (block rows) */
+  int32_t C;      /* input channels Ch */
+  int32_t H;      /* input side (square) */
+  int32_t M;      /* kernels (block columns) */
+  int32_t R;      /* kernel side (square) */
+  int32_t stride; /* U */
+  int32_t pad;
+  int32_t groups;
+  int32_t bias_enabled;
+} ftc_conv_desc;
+
+/* LayerPlan, workflow.hpp:23-29 */
+typedef struct ftc_plan {
+  int32_t rc_enabled;
+  int32_t clc_enabled;
+  double tau;
+  double t0, t1, t2, p_r;
+} ftc_plan;
+
+/* Fault injection.  std::function FaultHooks (workflow.hpp:117-121) cannot cross
+ * an ABI or run on a device; they become a POD list (fault.hpp:42-53, 111-172):
+ *   target OUTPUT  = post_conv: applied inside the conv epilogue, before O is
+ *                    stored and before the fused summations read it;
+ *   target FMAP/KERNEL/CD1/CD2/CW1/CW2 = pre_conv: applied to the layer's working
+ *                    copies after the input checksums were taken.
+ * Coordinates: OUTPUT (n, m, x, y); FMAP (n, c=m, x, y); KERNEL (m=n, c=m, i=x, j=y)
+ * i.e. index = ((n*d1 + m)*d2 + x)*d3 + y of the target tensor; the CD1/CD2/CW1/CW2
+ * targets use n = 0.
+ * A negative coordinate means "all" along that axis (output_block/row/column).
+ * Modes: BITFLIP flips bit (bit % 31) of the FP32 word (fault.hpp:82-87; on the
+ * FP64 checksums bit % 63); ADD adds value + n_coef*n + m_coef*m; SET stores value. */
+typedef enum ftc_fault_target {
+  FTC_FAULT_OUTPUT = 0, FTC_FAULT_FMAP = 1, FTC_FAULT_KERNEL = 2,
+  FTC_FAULT_CD1 = 3, FTC_FAULT_CD2 = 4, FTC_FAULT_CW1 = 5, FTC_FAULT_CW2 = 6
+} ftc_fault_target;
+typedef enum ftc_fault_mode { FTC_FAULT_BITFLIP = 0, FTC_FAULT_ADD = 1, FTC_FAULT_SET = 2 } ftc_fault_mode;
+typedef struct ftc_fault {
+  int32_t target;
+  int32_t mode;
+  int32_t n, m, x, y;
+  uint32_t bit;
+  float value;
+  float n_coef, m_coef;
+} ftc_fault;
+
+/* LayerReport, report.hpp:38-47, as POD (fixed-capacity vectors). */
+typedef struct ftc_layer_report {
+  int32_t detected;
+  int32_t stage;            /* ftc_stage */
+  int32_t weights_reloaded;
+  int32_t recomputed;
+  int32_t n_blocks;         /* total corrected blocks; first FTC_MAX_BLOCKS listed */
+  int32_t blocks[FTC_MAX_BLOCKS][2]; /* (i, j) = (n, m), ascending */
+  int32_t n_stages;
+  int32_t stages[FTC_MAX_STAGES];    /* stages_attempted */
+  double max_rel_dev;       /* DetectionResult::max_rel_dev (schemes.hpp:21) of CoC-D */
+  int32_t n_flagged;        /* CoC-D mismatching positions */
+  int32_t repaired_planes;  /* (n,m) planes recomputed on device */
+  double t_detect_ms;       /* host-measured wall time of the clean path */
+  double t_total_ms;        /* host-measured wall time including the error path */
+} ftc_layer_report;
+
+typedef struct ftc_layer ftc_layer;
+
+/* ---------------------------------------------------------------- library */
+int32_t ftc_abi_version(void);
+const char* ftc_last_error(void);
+/* Device conv engine: 0 = tcgen05 3xTF32 implicit GEMM (default), 1 = FP32 SIMT
+ * direct conv.  Both are hand-written sm_100a kernels; there is no CPU path. */
+int ftc_set_conv_engine(int engine);
+int ftc_get_conv_engine(void);
+
+/* output_extent, tensor.hpp:100-107 (ConfigError unless integral) */
+int ftc_output_extent(int32_t H, int32_t R, int32_t pad, int32_t stride, int32_t* E);
+
+/* ---------------------------------------------------------------- layer */
+/* build_model's per-layer work (model.hpp:77-108): validates shapes
+ * (conv.hpp:16-26), uploads the golden W and bias, precomputes the golden kernel
+ * checksums Cw1/Cw2 on device (model.hpp:104, checksums.hpp:70-88) and the packed
+ * tensor-core operands.  W_host/bias_host are HOST pointers (bias may be NULL). */
+int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float* bias_host,
+                     ftc_layer** out);
+int ftc_layer_destroy(ftc_layer* layer);
+int ftc_layer_extent(const ftc_layer* layer, int32_t* E);
+
+/* conv_forward(D, W, bias, p) (conv.hpp:114-131) with the layer's golden W. */
+int ftc_conv_forward(ftc_layer* layer, const float* D, float* O, void* stream);
+
+/* run_protected_layer (workflow.hpp:141-339): CoC-D detection; on a mismatch
+ * kernel verify/reload, CoC -> [RC] -> [ClC] -> FC -> recompute, all evaluated on
+ * device, and the corrected (n,m) planes recomputed on device.  Blocks until the
+ * report is final.  Returns FTC_INTEGRITY_ERROR when recompute fails twice. */
+int ftc_protected_conv(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                       const ftc_fault* faults, int32_t n_faults, ftc_layer_report* report,
+                       void* stream);
+
+/* Same as ftc_protected_conv with HOST input/output buffers (the reference's own
+ * calling convention: run_protected_layer takes and returns host tensors).  The
+ * host<->device copies run on `stream`. */
+int ftc_protected_conv_host(ftc_layer* layer, const ftc_plan* plan, const float* D_host,
+                            float* O_host, const ftc_fault* faults, int32_t n_faults,
+                            ftc_layer_report* report, void* stream);
+
+/* Split form for pipelines: _launch enqueues the clean path (checksums, conv with
+ * fused summations, CoC-D) without blocking; _finish waits for it, runs the error
+ * path if CoC-D fired and fills the report.  Between the two calls D and O must
+ * stay valid. */
+int ftc_protected_conv_launch(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                              const ftc_fault* faults, int32_t n_faults, void* stream);
+int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
+
+/* Instrumentation for bench.py: when enabled, CUDA events bracket the conv kernel
+ * of every protected/unprotected call on its launching stream; _kernel_time
+ * returns the accumulated device time (ms) and launch count (reset if `reset`).
+ * ftc_kernel_launches counts every kernel this library has launched. */
+int ftc_layer_set_timing(ftc_layer* layer, int32_t enable);
+int ftc_layer_kernel_time(ftc_layer* layer, double* conv_ms, int32_t* conv_launches,
+                          int32_t reset);
+uint64_t ftc_kernel_launches(void);
+
+/* ---------------------------------------------------------------- building blocks
+ * Device implementations of checksums.hpp / schemes.hpp primitives, FP64,
+ * summed in the reference's association order (bitwise equal to the reference at
+ * T=double on the same FP32 data).  All pointers are device pointers. */
+
+/* input_checksums (checksums.hpp:91-113): Cd1 = sum_n D_n, Cd2 = sum_n n*D_n, C*H*H each */
+int ftc_input_checksums(const ftc_conv_desc* desc, const float* D, double* cd1, double* cd2,
+                        void* stream);
+/* kernel_checksums (checksums.hpp:70-88): C*R*R each (groups concatenated) */
+int ftc_kernel_checksums(const ftc_conv_desc* desc, const float* W, double* cw1, double* cw2,
+                         void* stream);
+/* output_checksums (checksums.hpp:134-161).  co[k] receives Co(k+1) when bit k of
+ * `which` is set: Co1,Co3 are M grids, Co2,Co4 N grids, Co5..7 one E x E grid. */
+int ftc_output_checksums(const ftc_conv_desc* desc, uint32_t which, const float* D, const float* W,
+                         const double* cd1, const double* cd2, const double* cw1,
+                         const double* cw2, double* const co[7], void* stream);
+/* output_summations (checksums.hpp:165-190) + BiasAdjuster (:195-245) if bias != NULL */
+int ftc_output_summations(int32_t N, int32_t M, int32_t E, const float* O, uint32_t which,
+                          const float* bias, double* const so[7], void* stream);
+/* detect_coc_d (schemes.hpp:79-94): writes the E2-byte mismatch mask (may be NULL) and
+ * returns clean / max_rel_dev through HOST pointers (synchronises `stream`). */
+int ftc_detect_coc_d(const double* co5, const double* so5, int32_t E2, double tau, uint8_t* mask,
+                     int32_t* clean, double* max_rel_dev, void* stream);
+/* verify_kernel (checksums.hpp:250-259); result through a HOST pointer. */
+int ftc_verify_kernel(const ftc_conv_desc* desc, const float* W, const double* cw1_ref, double tau,
+                      int32_t* ok, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTC_ABI_H */

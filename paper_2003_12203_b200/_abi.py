@@ -1,0 +1,95 @@
+"""ctypes binding of include/ftc_abi.h (libftconv_b200.so).
+
+The library is REQUIRED: importing the compute entry points without it raises.
+There is no CPU path; every call lands in hand-written sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libftconv_b200.so")
+
+MAX_BLOCKS = 4096
+MAX_STAGES = 8
+
+# every symbol include/ftc_abi.h declares (checked by tests/test_abi_symbols.py)
+EXPORTS = (
+    "ftc_abi_version", "ftc_last_error", "ftc_set_conv_engine", "ftc_get_conv_engine",
+    "ftc_output_extent", "ftc_layer_create", "ftc_layer_destroy", "ftc_layer_extent",
+    "ftc_conv_forward", "ftc_protected_conv", "ftc_protected_conv_host",
+    "ftc_protected_conv_launch", "ftc_protected_conv_finish", "ftc_input_checksums",
+    "ftc_kernel_checksums", "ftc_output_checksums", "ftc_output_summations", "ftc_detect_coc_d",
+    "ftc_verify_kernel", "ftc_layer_set_timing", "ftc_layer_kernel_time", "ftc_kernel_launches",
+)
+
+
+class ConvDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("N", "C", "H", "M", "R", "stride", "pad", "groups",
+                                         "bias_enabled")]
+
+
+class Plan(C.Structure):
+    _fields_ = [("rc_enabled", C.c_int32), ("clc_enabled", C.c_int32), ("tau", C.c_double),
+                ("t0", C.c_double), ("t1", C.c_double), ("t2", C.c_double), ("p_r", C.c_double)]
+
+
+class Fault(C.Structure):
+    _fields_ = [("target", C.c_int32), ("mode", C.c_int32), ("n", C.c_int32), ("m", C.c_int32),
+                ("x", C.c_int32), ("y", C.c_int32), ("bit", C.c_uint32), ("value", C.c_float),
+                ("n_coef", C.c_float), ("m_coef", C.c_float)]
+
+
+class Report(C.Structure):
+    _fields_ = [("detected", C.c_int32), ("stage", C.c_int32), ("weights_reloaded", C.c_int32),
+                ("recomputed", C.c_int32), ("n_blocks", C.c_int32),
+                ("blocks", (C.c_int32 * 2) * MAX_BLOCKS), ("n_stages", C.c_int32),
+                ("stages", C.c_int32 * MAX_STAGES), ("max_rel_dev", C.c_double),
+                ("n_flagged", C.c_int32), ("repaired_planes", C.c_int32),
+                ("t_detect_ms", C.c_double), ("t_total_ms", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library; fail loudly if it was not built (no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: run `python paper_2003_12203_b200/build.py` "
+                "(or __graft_entry__.build()); this package has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, u32, dbl = C.c_void_p, C.c_int32, C.c_uint32, C.c_double
+        L.ftc_last_error.restype = C.c_char_p
+        L.ftc_abi_version.restype = i32
+        L.ftc_layer_create.argtypes = [C.POINTER(ConvDesc), vp, vp, C.POINTER(vp)]
+        L.ftc_layer_destroy.argtypes = [vp]
+        L.ftc_layer_extent.argtypes = [vp, C.POINTER(i32)]
+        L.ftc_output_extent.argtypes = [i32, i32, i32, i32, C.POINTER(i32)]
+        L.ftc_conv_forward.argtypes = [vp, vp, vp, vp]
+        L.ftc_protected_conv.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32,
+                                         C.POINTER(Report), vp]
+        L.ftc_protected_conv_host.argtypes = L.ftc_protected_conv.argtypes
+        L.ftc_protected_conv_launch.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32,
+                                                vp]
+        L.ftc_protected_conv_finish.argtypes = [vp, C.POINTER(Report)]
+        L.ftc_input_checksums.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp]
+        L.ftc_kernel_checksums.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp]
+        L.ftc_output_checksums.argtypes = [C.POINTER(ConvDesc), u32, vp, vp, vp, vp, vp, vp,
+                                           C.POINTER(vp), vp]
+        L.ftc_output_summations.argtypes = [i32, i32, i32, vp, u32, vp, C.POINTER(vp), vp]
+        L.ftc_detect_coc_d.argtypes = [vp, vp, i32, dbl, vp, C.POINTER(i32), C.POINTER(dbl), vp]
+        L.ftc_verify_kernel.argtypes = [C.POINTER(ConvDesc), vp, vp, dbl, C.POINTER(i32), vp]
+        L.ftc_set_conv_engine.argtypes = [C.c_int]
+        L.ftc_layer_set_timing.argtypes = [vp, i32]
+        L.ftc_layer_kernel_time.argtypes = [vp, C.POINTER(dbl), C.POINTER(i32), i32]
+        L.ftc_kernel_launches.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().ftc_last_error().decode(errors="replace")

@@ -1,0 +1,385 @@
+// ftc_checksums.cu -- FP64 checksum, summation and CoC-D kernels.
+//
+// Everything the error path consumes is computed in the reference's association
+// order (one thread owns one output and walks the reduced index ascending), so at
+// T=double the results are bitwise equal to checksums.hpp on the same FP32 data;
+// the clean-path detection (Co5 fast, fused So5) trades that for parallelism.
+#include <cuda_runtime.h>
+
+#include "ftc_common.cuh"
+
+namespace ftc {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int blocks_for(long long n, int threads = kThreads) {
+  long long b = (n + threads - 1) / threads;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// ------------------------------------------------------------------ K2: input_checksums
+// checksums.hpp:100-107.  Thread = 4 consecutive (k,a,b) positions; the batch loop
+// is fully independent across n (loads in flight) and accumulates n ascending.
+// HBM-bound: reads |D|, writes 2 x C*H*H doubles.
+__global__ void __launch_bounds__(kThreads) k_input_checksums_v4(const float* __restrict__ D, int N,
+                                                                 long long per4,
+                                                                 double* __restrict__ cd1,
+                                                                 double* __restrict__ cd2) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per4) return;
+  const float4* src = reinterpret_cast<const float4*>(D) + e;
+  double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+  int n = 0;
+  for (; n + 4 <= N; n += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (long long)(n + u) * per4);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double w = (double)(n + u);
+      const double a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s1[q] = dadd(s1[q], a[q]);
+        s2[q] = dadd(s2[q], dmul(w, a[q]));
+      }
+    }
+  }
+  for (; n < N; ++n) {
+    const float4 v = __ldcs(src + (long long)n * per4);
+    const double w = (double)n;
+    const double a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s1[q] = dadd(s1[q], a[q]);
+      s2[q] = dadd(s2[q], dmul(w, a[q]));
+    }
+  }
+  double2* o1 = reinterpret_cast<double2*>(cd1) + 2 * e;
+  double2* o2 = reinterpret_cast<double2*>(cd2) + 2 * e;
+  o1[0] = make_double2(s1[0], s1[1]);
+  o1[1] = make_double2(s1[2], s1[3]);
+  o2[0] = make_double2(s2[0], s2[1]);
+  o2[1] = make_double2(s2[2], s2[3]);
+}
+
+__global__ void k_input_checksums_scalar(const float* __restrict__ D, int N, long long per,
+                                         double* __restrict__ cd1, double* __restrict__ cd2) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per) return;
+  double s1 = 0.0, s2 = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double v = D[(long long)n * per + e];
+    s1 = dadd(s1, v);
+    s2 = dadd(s2, dmul((double)n, v));
+  }
+  cd1[e] = s1;
+  cd2[e] = s2;
+}
+
+// ------------------------------------------------------------------ K3: kernel_checksums
+// checksums.hpp:78-87: position (g*Ckw + k, i, j) sums kernels m of group g ascending
+// with the GLOBAL index m as weight.
+__global__ void k_kernel_checksums(const float* __restrict__ W, int M, int Ckw, int R, int groups,
+                                   double* __restrict__ cw1, double* __restrict__ cw2) {
+  const int per = Ckw * R * R;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per * groups) return;
+  const int g = e / per, r = e % per, mpg = M / groups;
+  double s1 = 0.0, s2 = 0.0;
+  for (int mg = 0; mg < mpg; ++mg) {
+    const int m = g * mpg + mg;
+    const double v = W[(long long)m * per + r];
+    s1 = dadd(s1, v);
+    s2 = dadd(s2, dmul((double)m, v));
+  }
+  cw1[e] = s1;
+  cw2[e] = s2;
+}
+
+// ------------------------------------------------------------------ K4: exact FP64 conv
+// conv_direct (conv.hpp:39-62) at T=double: one thread per output, (k,i,j) ascending,
+// padded taps contribute 0*w exactly like padded_at (:28-37).
+template <typename TI, typename TW>
+__global__ void k_conv_f64_exact(const TI* __restrict__ in, const TW* __restrict__ w,
+                                 double* __restrict__ out, int B, int Cin, int H, int Mo, int Ckw,
+                                 int R, int U, int pad, int groups, int E) {
+  const long long total = (long long)B * Mo * E * E;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int y = (int)(idx % E);
+  const int x = (int)((idx / E) % E);
+  const int mo = (int)((idx / ((long long)E * E)) % Mo);
+  const int b = (int)(idx / ((long long)E * E * Mo));
+  const int mpg = Mo / groups;
+  const int kbase = (mo / mpg) * Ckw;
+  const TI* src = in + ((long long)b * Cin + kbase) * H * H;
+  const TW* ker = w + (long long)mo * Ckw * R * R;
+  double acc = 0.0;
+  for (int k = 0; k < Ckw; ++k)
+    for (int i = 0; i < R; ++i) {
+      const int hh = U * x + i - pad;
+      const bool rok = hh >= 0 && hh < H;
+      for (int j = 0; j < R; ++j) {
+        const int ww = U * y + j - pad;
+        double v = 0.0;
+        if (rok && ww >= 0 && ww < H) v = (double)src[((long long)k * H + hh) * H + ww];
+        acc = dadd(acc, dmul(v, (double)ker[(k * R + i) * R + j]));
+      }
+    }
+  out[idx] = acc;
+}
+
+// Co5 = conv_block(Cd1, Cw1) for the clean path: one warp per output position,
+// lanes stride over K, fixed xor-shuffle tree (deterministic run to run).
+__global__ void k_co5_fast(const double* __restrict__ cd1, const double* __restrict__ cw1,
+                           double* __restrict__ co5, int C, int H, int R, int U, int pad, int E) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= E * E) return;
+  const int x = warp / E, y = warp % E;
+  const int RR = R * R, K = C * RR;
+  double acc = 0.0;
+  for (int k = lane; k < K; k += 32) {
+    const int c = k / RR, t = k % RR, i = t / R, j = t % R;
+    const int hh = U * x + i - pad, ww = U * y + j - pad;
+    if (hh >= 0 && hh < H && ww >= 0 && ww < H)
+      acc = fma(cd1[((long long)c * H + hh) * H + ww], cw1[k], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) co5[warp] = acc;
+}
+
+// BiasAdjuster ctor (checksums.hpp:199-208) at T=double
+__global__ void k_bias_aggregates(const float* __restrict__ b, int M, double* agg) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double sb = 0.0, smb = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double v = b[m];
+    sb = dadd(sb, v);
+    smb = dadd(smb, dmul((double)m, v));
+  }
+  agg[0] = sb;
+  agg[1] = smb;
+}
+
+// ------------------------------------------------------------------ K5: output_summations
+__device__ __forceinline__ double vo(const VirtualO& v, long long i) {
+  if (v.present && v.present[i]) return v.ov[i];
+  return (double)v.O[i];
+}
+
+// So1/So3 (per column m, n ascending) + bias rows (checksums.hpp:212-220)
+__global__ void k_sum_cols(VirtualO v, int N, int M, int E2, uint32_t which, const float* bias,
+                           double* so1, double* so3) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)M * E2) return;
+  const int m = (int)(q / E2), f = (int)(q % E2);
+  double s1 = 0.0, s3 = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double x = vo(v, ((long long)n * M + m) * E2 + f);
+    s1 = dadd(s1, x);
+    s3 = dadd(s3, dmul((double)n, x));
+  }
+  if (bias) {
+    const double b = bias[m];
+    s1 = dsub(s1, dmul((double)N, b));
+    s3 = dsub(s3, dmul((double)((long long)N * (N - 1) / 2), b));
+  }
+  if (which & FTC_CK_O1) so1[q] = s1;
+  if (which & FTC_CK_O3) so3[q] = s3;
+}
+
+// So2/So4 (per row n, m ascending) (checksums.hpp:215-223)
+__global__ void k_sum_rows(VirtualO v, int N, int M, int E2, uint32_t which, const double* agg,
+                           double* so2, double* so4) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)N * E2) return;
+  const int n = (int)(q / E2), f = (int)(q % E2);
+  double s2 = 0.0, s4 = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double x = vo(v, ((long long)n * M + m) * E2 + f);
+    s2 = dadd(s2, x);
+    s4 = dadd(s4, dmul((double)m, x));
+  }
+  if (agg) {
+    s2 = dsub(s2, agg[0]);
+    s4 = dsub(s4, agg[1]);
+  }
+  if (which & FTC_CK_O2) so2[q] = s2;
+  if (which & FTC_CK_O4) so4[q] = s4;
+}
+
+// So5/So6/So7 (per position, (n,m) ascending) (checksums.hpp:224-229)
+__global__ void k_sum_total(VirtualO v, int N, int M, int E2, uint32_t which, const double* agg,
+                            double* so5, double* so6, double* so7) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= E2) return;
+  double s5 = 0.0, s6 = 0.0, s7 = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double wn = (double)n;
+    const long long base = (long long)n * M * E2 + f;
+    for (int m = 0; m < M; ++m) {
+      const double x = vo(v, base + (long long)m * E2);
+      s5 = dadd(s5, x);
+      s6 = dadd(s6, dmul((double)m, x));
+      s7 = dadd(s7, dmul(wn, x));
+    }
+  }
+  if (agg) {
+    const double nN = (double)N, wnn = (double)((long long)N * (N - 1) / 2);
+    s5 = dsub(s5, dmul(nN, agg[0]));
+    s6 = dsub(s6, dmul(nN, agg[1]));
+    s7 = dsub(s7, dmul(wnn, agg[0]));
+  }
+  if (which & FTC_CK_O5) so5[f] = s5;
+  if (which & FTC_CK_O6) so6[f] = s6;
+  if (which & FTC_CK_O7) so7[f] = s7;
+}
+
+// ------------------------------------------------------------------ K6: CoC-D
+__device__ __forceinline__ void detect_one(double c, double s, double tau, int* flagged,
+                                           unsigned long long* mrd_bits, bool* bad) {
+  double den = fabs(c);
+  if (den < fabs(s)) den = fabs(s);
+  if (den < 1.0) den = 1.0;
+  const double dev = fabs(c - s) / den;
+  // std::max(a,b) = a<b?b:a ignores NaN devs; non-negative doubles order as u64
+  if (dev == dev && dev > 0.0) atomicMax(mrd_bits, (unsigned long long)__double_as_longlong(dev));
+  *bad = values_differ(c, s, tau);
+  if (*bad) atomicAdd(flagged, 1);
+}
+
+__global__ void k_detect_fast(const double* __restrict__ co5, const double* __restrict__ rowsum,
+                              int N, int E2, int bias, const double* agg, double tau,
+                              DetectStats* st) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= E2) return;
+  double s = 0.0;
+  for (int n = 0; n < N; ++n) s += rowsum[(long long)n * E2 + f];
+  if (bias) s -= (double)N * agg[0];
+  bool bad;
+  detect_one(co5[f], s, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
+}
+
+__global__ void k_detect_exact(const double* __restrict__ co5, const double* __restrict__ so5,
+                               int E2, double tau, uint8_t* mask, DetectStats* st) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= E2) return;
+  bool bad;
+  detect_one(co5[f], so5[f], tau, &st->flagged, &st->max_rel_dev_bits, &bad);
+  if (mask) mask[f] = bad ? 1 : 0;
+}
+
+__global__ void k_count_differ(const double* __restrict__ c, const double* __restrict__ s,
+                               long long n, double tau, int* count) {
+  int local = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (values_differ(c[i], s[i], tau)) ++local;
+  if (local) atomicAdd(count, local);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int launch_input_checksums(const float* D, int N, long long per, double* cd1, double* cd2,
+                           cudaStream_t s) {
+  const bool vec = (per % 4 == 0) && ((uintptr_t)D % 16 == 0) && ((uintptr_t)cd1 % 16 == 0) &&
+                   ((uintptr_t)cd2 % 16 == 0);
+  if (vec)
+    FTC_LAUNCH(k_input_checksums_v4<<<blocks_for(per / 4), kThreads, 0, s>>>(D, N, per / 4, cd1, cd2));
+  else
+    FTC_LAUNCH(k_input_checksums_scalar<<<blocks_for(per), kThreads, 0, s>>>(D, N, per, cd1, cd2));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, double* cw1,
+                            double* cw2, cudaStream_t s) {
+  const int n = Ckw * R * R * groups;
+  FTC_LAUNCH(k_kernel_checksums<<<blocks_for(n), kThreads, 0, s>>>(W, M, Ckw, R, groups, cw1, cw2));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64, double* out,
+                          int B, int Cin, int H, int Mo, int Ckw, int R, int U, int pad,
+                          int groups, int E, cudaStream_t s) {
+  const long long total = (long long)B * Mo * E * E;
+  const int g = blocks_for(total, 128);
+  if (in_f64 && w_f64)
+    FTC_LAUNCH(k_conv_f64_exact<double, double><<<g, 128, 0, s>>>((const double*)in, (const double*)w, out, B,
+                                                       Cin, H, Mo, Ckw, R, U, pad, groups, E));
+  else if (in_f64)
+    FTC_LAUNCH(k_conv_f64_exact<double, float><<<g, 128, 0, s>>>((const double*)in, (const float*)w, out, B,
+                                                      Cin, H, Mo, Ckw, R, U, pad, groups, E));
+  else if (w_f64)
+    FTC_LAUNCH(k_conv_f64_exact<float, double><<<g, 128, 0, s>>>((const float*)in, (const double*)w, out, B,
+                                                      Cin, H, Mo, Ckw, R, U, pad, groups, E));
+  else
+    FTC_LAUNCH(k_conv_f64_exact<float, float><<<g, 128, 0, s>>>((const float*)in, (const float*)w, out, B,
+                                                     Cin, H, Mo, Ckw, R, U, pad, groups, E));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_co5_fast(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
+                    int pad, int E, cudaStream_t s) {
+  const long long threads = (long long)E * E * 32;
+  FTC_LAUNCH(k_co5_fast<<<blocks_for(threads), kThreads, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s) {
+  FTC_LAUNCH(k_bias_aggregates<<<1, 32, 0, s>>>(bias, M, agg));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t which,
+                             const float* bias, const double* agg, double* const so[7],
+                             cudaStream_t s) {
+  const int E2 = E * E;
+  if (which & (FTC_CK_O1 | FTC_CK_O3))
+    FTC_LAUNCH(k_sum_cols<<<blocks_for((long long)M * E2), kThreads, 0, s>>>(v, N, M, E2, which, bias, so[0],
+                                                                   so[2]));
+  if (which & (FTC_CK_O2 | FTC_CK_O4))
+    FTC_LAUNCH(k_sum_rows<<<blocks_for((long long)N * E2), kThreads, 0, s>>>(v, N, M, E2, which,
+                                                                   bias ? agg : nullptr, so[1],
+                                                                   so[3]));
+  if (which & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7))
+    FTC_LAUNCH(k_sum_total<<<blocks_for(E2, 64), 64, 0, s>>>(v, N, M, E2, which, bias ? agg : nullptr, so[4],
+                                                  so[5], so[6]));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_fast(const double* co5, const double* rowsum, int N, int E2, int bias,
+                       const double* agg, double tau, DetectStats* st, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_fast<<<blocks_for(E2), kThreads, 0, s>>>(co5, rowsum, N, E2, bias, agg, tau, st));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
+                        DetectStats* st, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_exact<<<blocks_for(E2), kThreads, 0, s>>>(co5, so5, E2, tau, mask, st));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_count_differ(const double* c, const double* s_, long long n, double tau, int* count,
+                        cudaStream_t s) {
+  int g = blocks_for(n);
+  if (g > 1184) g = 1184;
+  FTC_LAUNCH(k_count_differ<<<g, kThreads, 0, s>>>(c, s_, n, tau, count));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+}  // namespace ftc

@@ -1,0 +1,217 @@
+// ftc_common.cuh -- shared device helpers and internal kernel interfaces of the
+// B200-native ABFT-protected convolution.  Reference paths are relative to
+// /root/reference/proj/core/include/ftconv/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ftc_abi.h"
+
+namespace ftc {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+  int code;
+  std::string msg;
+};
+void set_error(int code, const std::string& msg);
+#define FTC_CUDA_CHECK(expr)                                                        \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      ::ftc::set_error(FTC_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      return FTC_CUDA_ERROR;                                                        \
+    }                                                                               \
+  } while (0)
+
+// every kernel launch of the library goes through FTC_LAUNCH so the launch
+// counter (ftc_kernel_launches) sees it
+void count_launch();
+#define FTC_LAUNCH(...)     \
+  do {                      \
+    __VA_ARGS__;            \
+    ::ftc::count_launch();  \
+  } while (0)
+
+// ------------------------------------------------------------------ device helpers
+// FP64 arithmetic of the checksum path goes through the _rn intrinsics so nvcc can
+// never contract a*b+c into an FMA: the association order AND the rounding of
+// every product match the reference at T=double (x86-64 SSE2, no FMA).
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// values_differ (checksums.hpp:54-60): |c-s| > tau*max(|c|,|s|,1) in double.
+// Any NaN -> false; inf vs anything -> inf > tau*inf -> false.
+__device__ __forceinline__ bool values_differ(double c, double s, double tau) {
+  const double cc = fabs(c), ss = fabs(s);
+  double m = cc;
+  if (m < ss) m = ss;
+  if (m < 1.0) m = 1.0;
+  return fabs(dsub(c, s)) > dmul(tau, m);
+}
+
+// locate_index (schemes.hpp:57-62).  llround of non-finite/huge values is
+// "integer indefinite" on x86 (-> rejected), reproduced by the range guard.
+__device__ __forceinline__ bool locate_index(double r, int n, int* out) {
+  if (!(fabs(r) < 4.0e18)) return false;
+  const long long i = llround(r);
+  if (fabs(dsub(r, (double)i)) > 0.01) return false;
+  if (i < 0 || i >= (long long)n) return false;
+  *out = (int)i;
+  return true;
+}
+
+// flip_bit (fault.hpp:82-93): sign bit excluded
+__device__ __forceinline__ float flip_bit_f32(float v, unsigned bit) {
+  return __uint_as_float(__float_as_uint(v) ^ (1u << (bit % 31u)));
+}
+
+// post_conv fault applied to one output element (inside conv epilogues)
+__device__ __forceinline__ float apply_output_faults(float v, int n, int m, int x, int y,
+                                                     const ftc_fault* f, int nf) {
+  for (int q = 0; q < nf; ++q) {
+    const ftc_fault& a = f[q];
+    if (a.target != FTC_FAULT_OUTPUT) continue;
+    if ((a.n >= 0 && a.n != n) || (a.m >= 0 && a.m != m) || (a.x >= 0 && a.x != x) ||
+        (a.y >= 0 && a.y != y))
+      continue;
+    if (a.mode == FTC_FAULT_BITFLIP)
+      v = flip_bit_f32(v, a.bit);
+    else if (a.mode == FTC_FAULT_ADD)
+      v = v + (a.value + a.n_coef * (float)n + a.m_coef * (float)m);
+    else
+      v = a.value;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------ conv engine
+struct ConvArgs {
+  const float* D;  // N x C x H x H
+  const float* W;  // M x Ckw x R x R (reference layout)
+  const float* bias;  // M or null
+  float* O;           // N x M x E x E
+  int N, C, H, M, R, U, pad, groups, E, Ckw;
+  const ftc_fault* faults;  // device list (post_conv OUTPUT faults), may be null
+  int nfaults;
+  double* rowsum;    // [N][E2] sum_m O (So2 before bias adjust), may be null
+  double* rowsum_m;  // [N][E2] sum_m m*O (So4 before bias adjust), may be null
+  const uint32_t* plane_mask;  // N*M bits: store only these planes (repair); null = all
+  int img_lo, img_hi;          // images to compute
+};
+
+int conv_simt_launch(const ConvArgs& a, cudaStream_t s);
+
+// tcgen05 engine: per-layer packed operands + launch
+struct TcPlan;
+int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cudaStream_t s);
+void tc_plan_destroy(TcPlan* p);
+bool tc_supported(const ftc_conv_desc& d);
+int conv_tc_launch(const TcPlan* p, const ConvArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------------------ checksum kernels
+// input_checksums (exact order)
+int launch_input_checksums(const float* D, int N, long long per, double* cd1, double* cd2,
+                           cudaStream_t s);
+// kernel_checksums (exact order)
+int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, double* cw1,
+                            double* cw2, cudaStream_t s);
+// exact-order FP64 conv: out[b][mo][x][y] = sum_{k,i,j} in[b][kbase+k] * w[mo][k][i][j]
+//  in: float (D) or double (checksums); w: float (W) or double (Cw)
+int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64, double* out,
+                          int B, int Cin, int H, int Mo, int Ckw, int R, int U, int pad,
+                          int groups, int E, cudaStream_t s);
+// Co5 for the clean path: warp-split K, fixed shuffle order (deterministic)
+int launch_co5_fast(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
+                    int pad, int E, cudaStream_t s);
+// bias aggregates: agg[0]=sum_b, agg[1]=sum_mb (BiasAdjuster ctor, checksums.hpp:199-208)
+int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s);
+
+struct VirtualO {  // FP32 O plus FP64 overrides left by the verifier's rollbacks
+  const float* O;
+  const double* ov;        // N*M*E2 or null
+  const uint8_t* present;  // N*M*E2 or null
+};
+// output_summations + BiasAdjuster (exact order)
+int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t which,
+                             const float* bias, const double* agg, double* const so[7],
+                             cudaStream_t s);
+// clean-path CoC-D: so5 = sum_n rowsum (bias adjusted) vs co5; stats into dev[0..]
+struct DetectStats {
+  int32_t flagged;
+  int32_t pad_;
+  unsigned long long max_rel_dev_bits;
+};
+int launch_detect_fast(const double* co5, const double* rowsum, int N, int E2, int bias,
+                       const double* agg, double tau, DetectStats* st, cudaStream_t s);
+int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
+                        DetectStats* st, cudaStream_t s);
+int launch_count_differ(const double* c, const double* s_, long long n, double tau, int* count,
+                        cudaStream_t s);
+
+// ------------------------------------------------------------------ scheme kernels
+struct SchemeResult {
+  int32_t status;     // see SchemeStatus
+  int32_t n_patches;
+  int32_t line;       // located row/column/index
+  int32_t invalid;
+  int32_t lmin, lmax; // located-index range among flags
+  int32_t any;
+  int32_t fail;       // verifier failure flag
+  int32_t nr, nc;     // FC: flagged row/column counts
+  int32_t r0, c0;     // FC: the single flagged row/column
+  int32_t m6, m7;     // CoC pattern flags
+  int32_t c5bad;      // FC: Co5 inconsistent somewhere
+  int32_t mode;       // patch source: 0 = column flags (row = line), 1 = row flags (col = line)
+};
+enum SchemeStatus {
+  SCH_VALID = 0,      // patches emitted, verifier pending
+  SCH_DISCARD = 1,
+  SCH_ESCALATE = 2,
+  SCH_EMPTY = 3,      // corrected with no blocks
+  SCH_PROBE_ROW0 = 4, // CoC pattern m6 && !m7
+  SCH_PROBE_COL0 = 5, // CoC pattern m7 && !m6
+};
+struct Patches {
+  int32_t* n;
+  int32_t* m;
+  int32_t* f;
+  double* d;
+  int32_t cap;
+};
+struct Fam {  // the 7 families (checksums c, summations s); null if absent
+  const double* c[7];
+  const double* s[7];
+};
+int run_coc_analyze(const Fam& F, int N, int M, int E2, double tau, SchemeResult* r,
+                    const Patches& p, cudaStream_t s);
+int run_line_analyze(const Fam& F, bool rc, int N, int M, int E2, double tau, SchemeResult* r,
+                     const Patches& p, cudaStream_t s);
+int run_fc_analyze(const Fam& F, int N, int M, int E2, double tau, SchemeResult* r,
+                   const Patches& p, uint8_t* colmask, uint8_t* rowmask, int32_t* colany,
+                   int32_t* rowany, cudaStream_t s);
+
+struct VerifyWS {
+  double* ov;
+  uint8_t* present;
+  uint8_t* touched5;  // E2
+  uint8_t* touched1;  // M*E2
+};
+// workflow.hpp:205-219 verifier emulated over the patch list (see ftc_schemes.cu)
+int run_verify(const Fam& F, unsigned trusted, const float* O, int N, int M, int E2, int bias,
+               const float* bias_dev, const double* agg, double tau, const Patches& p,
+               const SchemeResult* r_dev, int np_host, const VerifyWS& ws, int32_t* fail,
+               cudaStream_t s);
+// rollback (schemes.hpp:71-74) in the FP64 override map, then clear the touch marks
+int run_rollback(const Patches& p, int np_host, int M, int E2, const VerifyWS& ws, cudaStream_t s);
+// plane mask (N*M bits) from the patch list
+int run_patch_planes(const Patches& p, int np_host, int M, uint32_t* mask, cudaStream_t s);
+// pre_conv faults on a float or double target
+int run_apply_faults(const ftc_fault* f_dev, int nf, int target, void* t, bool is_f64, int d1,
+                     int d2, int d3, long long count, cudaStream_t s);
+
+}  // namespace ftc

@@ -1,0 +1,378 @@
+"""Reference-shaped Python API over the C ABI (names mirror proj/core/include/ftconv/).
+
+    ConvParams, LayerPlan, LayerReport, ResolveStage      (tensor.hpp, workflow.hpp, report.hpp)
+    ShapeError, ConfigError, IoError, IntegrityError      (errors.hpp)
+    output_extent, conv_forward, run_protected_layer      (tensor.hpp, conv.hpp, workflow.hpp)
+    input_checksums, kernel_checksums, output_checksums,
+    output_summations, detect_coc_d, verify_kernel        (checksums.hpp, schemes.hpp)
+    FaultSpec helpers -> ftc_fault lists                  (fault.hpp)
+    ProtectedConv: a layer handle (the per-layer state build_model precomputes)
+
+Device tensors are torch CUDA tensors (torch is plumbing for memory and streams);
+numpy arrays are accepted by the *_host entry points.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+
+STAGES = ["none", "reload", "coc", "rc", "clc", "fc", "discard", "recompute"]
+
+
+class FtcError(RuntimeError):
+    pass
+
+
+class ShapeError(FtcError):
+    pass
+
+
+class ConfigError(FtcError):
+    pass
+
+
+class IoError(FtcError):
+    pass
+
+
+class IntegrityError(FtcError):
+    pass
+
+
+class CudaError(FtcError):
+    pass
+
+
+_ERRS = {1: ShapeError, 2: ConfigError, 3: IoError, 4: IntegrityError, 5: CudaError, 6: ValueError}
+
+
+def _check(status: int, what: str):
+    if status:
+        raise _ERRS.get(status, FtcError)(f"{what}: {_abi.last_error()}")
+
+
+@dataclass
+class ConvParams:
+    """tensor.hpp:92-97"""
+    stride: int = 1
+    groups: int = 1
+    pad: int = 0
+    bias_enabled: bool = False
+
+
+@dataclass
+class LayerPlan:
+    """workflow.hpp:23-29"""
+    rc_enabled: bool = True
+    clc_enabled: bool = False
+    tau: float = 1e-4
+    t0: float = 0.0
+    t1: float = 0.0
+    t2: float = 0.0
+    p_r: float = 0.5
+
+    def c(self) -> _abi.Plan:
+        return _abi.Plan(int(self.rc_enabled), int(self.clc_enabled), self.tau, self.t0, self.t1,
+                         self.t2, self.p_r)
+
+
+@dataclass
+class LayerReport:
+    """report.hpp:38-47 (+ device-side diagnostics)"""
+    layer: str = ""
+    detected: bool = False
+    stage: str = "none"
+    weights_reloaded: bool = False
+    recomputed: bool = False
+    corrected_blocks: list = field(default_factory=list)
+    stages_attempted: list = field(default_factory=list)
+    max_rel_dev: float = 0.0
+    n_flagged: int = 0
+    n_blocks: int = 0
+    repaired_planes: int = 0
+    timings: dict = field(default_factory=dict)
+
+    @staticmethod
+    def from_c(r: _abi.Report) -> "LayerReport":
+        nb = min(r.n_blocks, _abi.MAX_BLOCKS)
+        return LayerReport(
+            detected=bool(r.detected), stage=STAGES[r.stage], weights_reloaded=bool(r.weights_reloaded),
+            recomputed=bool(r.recomputed),
+            corrected_blocks=[(r.blocks[b][0], r.blocks[b][1]) for b in range(nb)],
+            stages_attempted=[STAGES[r.stages[s]] for s in range(r.n_stages)],
+            max_rel_dev=r.max_rel_dev, n_flagged=r.n_flagged, n_blocks=r.n_blocks,
+            repaired_planes=r.repaired_planes,
+            timings={"detect_ms": r.t_detect_ms, "total_ms": r.t_total_ms})
+
+    def verdict(self) -> dict:
+        return {"detected": self.detected, "stage": self.stage,
+                "weights_reloaded": self.weights_reloaded, "recomputed": self.recomputed,
+                "corrected_blocks": list(self.corrected_blocks),
+                "stages_attempted": list(self.stages_attempted)}
+
+
+# ----------------------------------------------------------------------------- faults (fault.hpp)
+TARGETS = {"output": 0, "fmap": 1, "kernel": 2, "cd1": 3, "cd2": 4, "cw1": 5, "cw2": 6}
+MODES = {"bitflip": 0, "add": 1, "set": 2}
+
+
+@dataclass
+class Fault:
+    """One injected fault (FaultSpec, fault.hpp:42-53, as a substitution the device applies)."""
+    target: str = "output"
+    n: int = -1
+    m: int = -1
+    x: int = -1
+    y: int = -1
+    mode: str = "bitflip"
+    bit: int = 23
+    value: float = 0.0
+    n_coef: float = 0.0
+    m_coef: float = 0.0
+
+    def c(self) -> _abi.Fault:
+        return _abi.Fault(TARGETS[self.target], MODES[self.mode], self.n, self.m, self.x, self.y,
+                          self.bit, self.value, self.n_coef, self.m_coef)
+
+
+def output_bitflip(n, m, x, y, bit) -> Fault:
+    return Fault("output", n, m, x, y, "bitflip", bit)
+
+
+def _faults_c(faults):
+    faults = list(faults or [])
+    arr = (_abi.Fault * max(1, len(faults)))()
+    for i, f in enumerate(faults):
+        arr[i] = f.c() if isinstance(f, Fault) else f
+    return arr, len(faults)
+
+
+# ----------------------------------------------------------------------------- helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return _torch().cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def output_extent(H: int, R: int, p: ConvParams) -> int:
+    """tensor.hpp:100-107"""
+    E = C.c_int32()
+    _check(_abi.lib().ftc_output_extent(H, R, p.pad, p.stride, C.byref(E)), "output_extent")
+    return E.value
+
+
+def desc(N, Cin, H, M, R, p: ConvParams) -> _abi.ConvDesc:
+    return _abi.ConvDesc(N, Cin, H, M, R, p.stride, p.pad, p.groups, int(p.bias_enabled))
+
+
+def set_conv_engine(name: str) -> None:
+    """'tc' (tcgen05 3xTF32, default) or 'simt' (FP32 FFMA)."""
+    _check(_abi.lib().ftc_set_conv_engine({"tc": 0, "simt": 1}[name]), "set_conv_engine")
+
+
+# ----------------------------------------------------------------------------- layer handle
+class ProtectedConv:
+    """One protected conv layer bound to a batch size: golden W/bias on device, golden
+    Cw1/Cw2 precomputed (model.hpp:104), packed tensor-core operands, scratch."""
+
+    def __init__(self, W: np.ndarray, bias: np.ndarray | None, p: ConvParams, N: int, H: int):
+        W = np.ascontiguousarray(W, np.float32)
+        if W.ndim != 4 or W.shape[2] != W.shape[3]:
+            raise ShapeError("kernel must be M x Ckw x R x R")
+        self.M, Ckw, self.R, _ = W.shape
+        self.C = Ckw * p.groups
+        self.N, self.H, self.p = N, H, p
+        if p.bias_enabled:
+            if bias is None or np.asarray(bias).size != self.M:
+                raise ShapeError("bias length must equal kernel count M")
+            bias = np.ascontiguousarray(np.asarray(bias).reshape(-1), np.float32)
+        else:
+            bias = None
+        self._W = W
+        self._bias = bias
+        self.desc = desc(N, self.C, H, self.M, self.R, p)
+        h = C.c_void_p()
+        _check(_abi.lib().ftc_layer_create(C.byref(self.desc), W.ctypes.data,
+                                           bias.ctypes.data if bias is not None else None,
+                                           C.byref(h)), "ftc_layer_create")
+        self.h = h
+        E = C.c_int32()
+        _abi.lib().ftc_layer_extent(self.h, C.byref(E))
+        self.E = E.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _abi.lib().ftc_layer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def out_shape(self):
+        return (self.N, self.M, self.E, self.E)
+
+    def _empty_out(self, D):
+        torch = _torch()
+        return torch.empty(self.out_shape, dtype=torch.float32, device=D.device)
+
+    def conv_forward(self, D, O=None, stream=None):
+        """conv_forward(D, W, bias, p) on device (conv.hpp:114-131)."""
+        O = self._empty_out(D) if O is None else O
+        _check(_abi.lib().ftc_conv_forward(self.h, _ptr(D), _ptr(O), _stream_ptr(stream)),
+               "ftc_conv_forward")
+        return O
+
+    def protected(self, D, plan: LayerPlan, faults=(), O=None, stream=None):
+        """run_protected_layer (workflow.hpp:141-339) on device tensors -> (O, LayerReport)."""
+        O = self._empty_out(D) if O is None else O
+        arr, n = _faults_c(faults)
+        rep = _abi.Report()
+        pl = plan.c()
+        st = _abi.lib().ftc_protected_conv(self.h, C.byref(pl), _ptr(D), _ptr(O), arr, n,
+                                           C.byref(rep), _stream_ptr(stream))
+        _check(st, "ftc_protected_conv")
+        return O, LayerReport.from_c(rep)
+
+    def launch(self, D, O, plan: LayerPlan, faults=(), stream=None):
+        arr, n = _faults_c(faults)
+        self._pl = plan.c()
+        _check(_abi.lib().ftc_protected_conv_launch(self.h, C.byref(self._pl), _ptr(D), _ptr(O), arr,
+                                                    n, _stream_ptr(stream)), "launch")
+
+    def finish(self) -> LayerReport:
+        rep = _abi.Report()
+        _check(_abi.lib().ftc_protected_conv_finish(self.h, C.byref(rep)), "finish")
+        return LayerReport.from_c(rep)
+
+    def protected_host(self, D: np.ndarray, plan: LayerPlan, faults=(), O: np.ndarray | None = None,
+                       stream=None):
+        """Host buffers in/out (the reference's calling convention)."""
+        D = np.ascontiguousarray(D, np.float32)
+        O = np.empty(self.out_shape, np.float32) if O is None else O
+        arr, n = _faults_c(faults)
+        rep = _abi.Report()
+        pl = plan.c()
+        st = _abi.lib().ftc_protected_conv_host(self.h, C.byref(pl), D.ctypes.data, O.ctypes.data,
+                                                arr, n, C.byref(rep),
+                                                0 if stream is None else _stream_ptr(stream))
+        _check(st, "ftc_protected_conv_host")
+        return O, LayerReport.from_c(rep)
+
+
+# ----------------------------------------------------------------------------- one-shot API
+def _to_dev(a):
+    torch = _torch()
+    if isinstance(a, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    return a.contiguous()
+
+
+def conv_forward(D, W, bias, p: ConvParams):
+    """conv.hpp:114-131 (device tensors or numpy in, torch CUDA tensor out)."""
+    Dd = _to_dev(D)
+    Wn = W.cpu().numpy() if hasattr(W, "cpu") else np.asarray(W)
+    bn = None if bias is None else (bias.cpu().numpy() if hasattr(bias, "cpu") else np.asarray(bias))
+    layer = ProtectedConv(Wn, bn, p, Dd.shape[0], Dd.shape[2])
+    try:
+        return layer.conv_forward(Dd)
+    finally:
+        torch = _torch()
+        torch.cuda.synchronize()
+        layer.close()
+
+
+def run_protected_layer(D, W, bias, p: ConvParams, plan: LayerPlan, faults=()):
+    """workflow.hpp:141-339 -> (O, LayerReport)."""
+    Dd = _to_dev(D)
+    Wn = W.cpu().numpy() if hasattr(W, "cpu") else np.asarray(W)
+    bn = None if bias is None else (bias.cpu().numpy() if hasattr(bias, "cpu") else np.asarray(bias))
+    layer = ProtectedConv(Wn, bn, p, Dd.shape[0], Dd.shape[2])
+    try:
+        return layer.protected(Dd, plan, faults)
+    finally:
+        layer.close()
+
+
+def input_checksums(D, W, groups: int, stream=None):
+    """checksums.hpp:91-113 -> (cd1, cd2, cw1, cw2) FP64 device tensors."""
+    torch = _torch()
+    N, Cin, H, _ = D.shape
+    M, Ckw, R, _ = W.shape
+    d = _abi.ConvDesc(N, Cin, H, M, R, 1, 0, groups, 0)
+    cd1 = torch.empty((Cin, H, H), dtype=torch.float64, device=D.device)
+    cd2 = torch.empty_like(cd1)
+    cw1 = torch.empty((Cin, R, R), dtype=torch.float64, device=D.device)
+    cw2 = torch.empty_like(cw1)
+    s = _stream_ptr(stream)
+    _check(_abi.lib().ftc_input_checksums(C.byref(d), _ptr(D), _ptr(cd1), _ptr(cd2), s), "input_checksums")
+    _check(_abi.lib().ftc_kernel_checksums(C.byref(d), _ptr(W), _ptr(cw1), _ptr(cw2), s), "kernel_checksums")
+    return cd1, cd2, cw1, cw2
+
+
+def output_checksums(which: int, D, W, ic, p: ConvParams, stream=None):
+    """checksums.hpp:134-161 -> list of 7 FP64 device tensors (None where not requested)."""
+    torch = _torch()
+    N, Cin, H, _ = D.shape
+    M, Ckw, R, _ = W.shape
+    E = output_extent(H, R, p)
+    d = desc(N, Cin, H, M, R, p)
+    shapes = [(M, E, E), (N, E, E), (M, E, E), (N, E, E), (E, E), (E, E), (E, E)]
+    out = [torch.empty(s, dtype=torch.float64, device=D.device) if which & (1 << k) else None
+           for k, s in enumerate(shapes)]
+    arr = (C.c_void_p * 7)(*[_ptr(o) or None for o in out])
+    cd1, cd2, cw1, cw2 = ic
+    _check(_abi.lib().ftc_output_checksums(C.byref(d), which, _ptr(D), _ptr(W), _ptr(cd1), _ptr(cd2),
+                                           _ptr(cw1), _ptr(cw2), arr, _stream_ptr(stream)),
+           "output_checksums")
+    return out
+
+
+def output_summations(O, which: int, bias=None, stream=None):
+    """checksums.hpp:165-245 -> list of 7 FP64 device tensors (bias-adjusted if bias given)."""
+    torch = _torch()
+    N, M, E, _ = O.shape
+    shapes = [(M, E, E), (N, E, E), (M, E, E), (N, E, E), (E, E), (E, E), (E, E)]
+    out = [torch.empty(s, dtype=torch.float64, device=O.device) if which & (1 << k) else None
+           for k, s in enumerate(shapes)]
+    arr = (C.c_void_p * 7)(*[_ptr(o) or None for o in out])
+    _check(_abi.lib().ftc_output_summations(N, M, E, _ptr(O), which, _ptr(bias), arr, _stream_ptr(stream)),
+           "output_summations")
+    return out
+
+
+def detect_coc_d(co5, so5, tau: float, stream=None):
+    """schemes.hpp:79-94 -> (clean, mismatch_mask (uint8 device), max_rel_dev)."""
+    torch = _torch()
+    mask = torch.empty(co5.numel(), dtype=torch.uint8, device=co5.device)
+    clean = C.c_int32()
+    mrd = C.c_double()
+    _check(_abi.lib().ftc_detect_coc_d(_ptr(co5), _ptr(so5), co5.numel(), tau, _ptr(mask), C.byref(clean),
+                                       C.byref(mrd), _stream_ptr(stream)), "detect_coc_d")
+    return bool(clean.value), mask, mrd.value
+
+
+def verify_kernel(W, cw1_ref, groups: int, tau: float, C_in: int | None = None, stream=None) -> bool:
+    """checksums.hpp:250-259"""
+    M, Ckw, R, _ = W.shape
+    d = _abi.ConvDesc(1, Ckw * groups, R, M, R, 1, 0, groups, 0)
+    ok = C.c_int32()
+    _check(_abi.lib().ftc_verify_kernel(C.byref(d), _ptr(W), _ptr(cw1_ref), tau, C.byref(ok),
+                                        _stream_ptr(stream)), "verify_kernel")
+    return bool(ok.value)
