@@ -254,12 +254,14 @@ __device__ __forceinline__ void detect_one(double c, double s, double tau, int* 
 }
 
 __global__ void k_detect_fast(const double* __restrict__ co5, const double* __restrict__ rowsum,
-                              int N, int E2, int bias, const double* agg, double tau,
+                              int parts, int N, int E2, int bias, const double* agg, double tau,
                               DetectStats* st) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= E2) return;
   double s = 0.0;
-  for (int n = 0; n < N; ++n) s += rowsum[(long long)n * E2 + f];
+  const long long slab = (long long)N * E2;
+  for (int n = 0; n < N; ++n)
+    for (int q = 0; q < parts; ++q) s += rowsum[q * slab + (long long)n * E2 + f];
   if (bias) s -= (double)N * agg[0];
   bool bad;
   detect_one(co5[f], s, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
@@ -359,9 +361,9 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
   return FTC_OK;
 }
 
-int launch_detect_fast(const double* co5, const double* rowsum, int N, int E2, int bias,
+int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s) {
-  FTC_LAUNCH(k_detect_fast<<<blocks_for(E2), kThreads, 0, s>>>(co5, rowsum, N, E2, bias, agg, tau, st));
+  FTC_LAUNCH(k_detect_fast<<<blocks_for(E2), kThreads, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -112,6 +112,7 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
 void tc_plan_destroy(TcPlan* p);
 bool tc_supported(const ftc_conv_desc& d);
 int conv_tc_launch(const TcPlan* p, const ConvArgs& a, cudaStream_t s);
+int tc_rowsum_parts(const TcPlan* p);  // N-tiles = row-sum partial slabs of N*E2
 
 // ------------------------------------------------------------------ checksum kernels
 // input_checksums (exact order)
@@ -146,7 +147,7 @@ struct DetectStats {
   int32_t pad_;
   unsigned long long max_rel_dev_bits;
 };
-int launch_detect_fast(const double* co5, const double* rowsum, int N, int E2, int bias,
+int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s);
 int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
                         DetectStats* st, cudaStream_t s);

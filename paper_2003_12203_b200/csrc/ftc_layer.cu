@@ -112,6 +112,7 @@ struct ftc_layer {
   const double *cw1 = nullptr, *cw2 = nullptr;
   float* O = nullptr;
   int nfaults = 0, n_out_faults = 0;
+  int rs_parts = 1;  // row-sum partial slabs written by the last fused-sum conv
   cudaStream_t stream = nullptr;
   std::chrono::steady_clock::time_point t0;
 };
@@ -154,7 +155,11 @@ int run_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults
   a.img_hi = img_hi;
   // The tensor-core engine packs the golden W once; a corrupted working W (kernel
   // fault injection) runs through the SIMT engine.
-  if (use_tc(L) && W == L->W) return conv_tc_launch(L->tc, a, s);
+  if (use_tc(L) && W == L->W) {
+    if (sums) L->rs_parts = tc_rowsum_parts(L->tc);
+    return conv_tc_launch(L->tc, a, s);
+  }
+  if (sums) L->rs_parts = 1;
   return conv_simt_launch(a, s);
 }
 
@@ -688,8 +693,7 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
       (st = dalloc(&L->cw2g, L->nCw)) || (st = dalloc(&L->cw1w, L->nCw)) ||
       (st = dalloc(&L->cw2w, L->nCw)) || (st = dalloc(&L->cd1, L->nCd)) ||
       (st = dalloc(&L->cd2, L->nCd)) || (st = dalloc(&L->co5f, L->E2)) ||
-      (st = dalloc(&L->rowsum, (size_t)desc->N * L->E2)) ||
-      (st = dalloc(&L->rowsum_m, (size_t)desc->N * L->E2)) || (st = dalloc(&L->stats, 1)))
+      (st = dalloc(&L->stats, 1)))
     return fail(st);
   if (cudaMallocHost((void**)&L->stats_h, sizeof(DetectStats)) != cudaSuccess)
     return fail(FTC_CUDA_ERROR);
@@ -712,6 +716,12 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
     return fail(FTC_CUDA_ERROR);
   if (tc_supported(*desc)) {
     if ((st = tc_plan_create(*desc, L->W, &L->tc, 0))) return fail(st);
+  }
+  {
+    const size_t parts = (size_t)tc_rowsum_parts(L->tc);
+    if ((st = dalloc(&L->rowsum, parts * desc->N * L->E2)) ||
+        (st = dalloc(&L->rowsum_m, parts * desc->N * L->E2)))
+      return fail(st);
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(FTC_CUDA_ERROR, "layer setup kernels failed");
@@ -820,7 +830,8 @@ int ftc_protected_conv_launch(ftc_layer* L, const ftc_plan* plan, const float* D
   CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
   FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
   FTC_CUDA_CHECK(cudaMemsetAsync(L->stats, 0, sizeof(DetectStats), s));
-  CK(launch_detect_fast(L->co5f, L->rowsum, d.N, L->E2, d.bias_enabled, L->agg, plan->tau, L->stats, s));
+  CK(launch_detect_fast(L->co5f, L->rowsum, L->rs_parts, d.N, L->E2, d.bias_enabled, L->agg, plan->tau,
+                        L->stats, s));
   FTC_CUDA_CHECK(cudaMemcpyAsync(L->stats_h, L->stats, sizeof(DetectStats), cudaMemcpyDeviceToHost, s));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
   L->inflight = true;
