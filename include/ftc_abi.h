@@ -208,6 +208,22 @@ int ftc_detect_coc_d(const double* co5, const double* so5, int32_t E2, double ta
 int ftc_verify_kernel(const ftc_conv_desc* desc, const float* W, const double* cw1_ref, double tau,
                       int32_t* ok, void* stream);
 
+/* ---------------------------------------------------------------- net glue
+ * Not reference interfaces: the reference chains convs directly (replay.hpp:14-25)
+ * and has no activation/pooling/residual ops; the BASELINE conv stacks need them
+ * between protected layers.  act: 0 none, 1 ReLU, 2 leaky-ReLU(0.1). */
+/* out = maxpool_{k,s,p}(act(in)); k = s = 1, p = 0 is a plain activation.  With
+ * in == out == NULL only the output side is returned in *Ho. */
+int ftc_glue_act_pool(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t act,
+                      int32_t k, int32_t s, int32_t p, int32_t* Ho, void* stream);
+/* out = act(a + b) elementwise over n values (b may be NULL) */
+int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act,
+                     void* stream);
+/* explicit zero pad of `lo` rows/cols at top/left and `hi` at bottom/right (hi < 0
+ * crops): expresses floor-mode strided convs through the exact extent rule */
+int ftc_glue_pad_crop(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t lo,
+                      int32_t hi, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

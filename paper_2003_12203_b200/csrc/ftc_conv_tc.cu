@@ -41,6 +41,7 @@ namespace ftc {
 struct TcPlan {
   int BN = 0, ntiles = 0, nkc = 0, K = 0, M = 0, G = 2;
   float* Wp = nullptr;  // [ntiles][nkc][2][BN][32], SW128-swizzled, hi then lo
+  int2* tab = nullptr;  // [nkc*32] im2col taps: {c*H*H + i*H + j, 1<<i | 1<<(16+j)}
 };
 
 namespace {
@@ -48,15 +49,17 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 32;
 constexpr int kStages = 4;
-constexpr int kThreads = 448;
-constexpr int kLoaderWarp = 4;
-constexpr int kMmaWarp = 5;
-constexpr int kEpiWarp0 = 6;
+constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
+constexpr int kLoaderWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr int kEpiWarp0 = 10;
 constexpr int kEpiThreads = 256;
+constexpr int kThreads = 576;
 
 struct TcArgs {
   const float* D;
   const float* Wp;
+  const int2* tab;
   const float* bias;
   float* O;
   int N, C, H, M, R, U, pad, E, K, nkc, BN, ntiles;
@@ -127,15 +130,12 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, "
-      "%31, %32};" ::"r"(taddr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};" ::"r"(taddr),
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
-      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
-      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 
@@ -169,17 +169,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t stage_bytes = (uint32_t)BN * 256u;  // hi + lo tiles, 128 B per row each
-  const uint32_t bar_base = sbase + kStages * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + kStages * stage_bytes);
+  int2* tab_s = reinterpret_cast<int2*>(sptr + kStages * stage_bytes);
+  const uint32_t tab_bytes = (uint32_t)a.nkc * kBK * 8u;
+  const uint32_t bar_base = sbase + kStages * stage_bytes + tab_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + kStages * stage_bytes + tab_bytes);
   // bars: full[4], empty[4], acc_full[2], acc_empty[2], then tmem base (u32)
   const uint32_t full0 = bar_base, empty0 = bar_base + 8 * kStages;
   const uint32_t accf0 = bar_base + 16 * kStages, acce0 = accf0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8 * s, 129);
+      mbar_init(full0 + 8 * s, kProdWarps * 32 + 1);
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -201,10 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const int E = a.E, E2 = E * E, H = a.H, R = a.R, RR = R * R, HH = H * H;
   const int ntile_total = a.ntiles * a.npt;
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
     // ================= A producers =================
-    const int r = threadIdx.x;  // row of the tile == TMEM lane
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // warp w owns TMEM lanes [32*(w%4), +32) (its pixels) and columns
+    // [16*(w/4), +16) of every K chunk; the im2col tap table (offset + validity bits)
+    // is a per-layer constant staged in shared memory.
+    const int q = warp & 3, hf = warp >> 2;
+    const int r = q * 32 + lane;  // row of the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t g = 0;
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
       const int pt = a.pt_lo + t % a.npt;
@@ -214,41 +221,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       const int f = valid ? (int)(p % E2) : 0;
       const int x = f / E, y = f - (f / E) * E;
       const int xb = x * a.U - a.pad, yb = y * a.U - a.pad;
-      const float* Dn = a.D + (long long)n * a.C * HH;
+      // validity of tap rows i / columns j for this pixel (bit i, bit 16+j)
+      uint32_t okmask = 0;
+      if (valid) {
+        for (int i = 0; i < R; ++i) {
+          if ((unsigned)(xb + i) < (unsigned)H) okmask |= 1u << i;
+          if ((unsigned)(yb + i) < (unsigned)H) okmask |= 1u << (16 + i);
+        }
+      }
+      const float* base = a.D + (long long)n * a.C * HH + (long long)xb * H + yb;
       for (int kc = 0; kc < a.nkc; ++kc, ++g) {
         const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-        // decode k0 = kc*32 into (c, i, j)
-        const int k0 = kc * kBK;
-        int c = k0 / RR;
-        int rem = k0 - c * RR;
-        int i = rem / R;
-        int j = rem - i * R;
-        float v[32];
+        const int2* tk = tab_s + kc * kBK + hf * 16;
+        float v[16];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int xx = xb + i, yy = yb + j;
-          const bool ok = valid && (c < a.C) && ((unsigned)xx < (unsigned)H) && ((unsigned)yy < (unsigned)H);
-          v[q] = ok ? __ldg(Dn + (long long)c * HH + xx * H + yy) : 0.f;
-          if (++j == R) {
-            j = 0;
-            if (++i == R) {
-              i = 0;
-              ++c;
-            }
-          }
+        for (int e = 0; e < 16; ++e) {
+          const int2 tp = tk[e];
+          const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+          v[e] = ok ? __ldg(base + tp.x) : 0.f;
         }
-        uint32_t hi[32], lo[32];
+        uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float h = tf32_rn(v[q]);
-          hi[q] = __float_as_uint(h);
-          lo[q] = __float_as_uint(tf32_rn(v[q] - h));
+        for (int e = 0; e < 16; ++e) {
+          // round-to-nearest TF32 in integer arithmetic (the tensor core reads the
+          // top 19 bits), lo = v - hi exact in FP32, rounded the same way
+          const uint32_t h = (__float_as_uint(v[e]) + 0x1000u) & 0xFFFFE000u;
+          hi[e] = h;
+          const float l = v[e] - __uint_as_float(h);
+          lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
         }
         mbar_wait(empty0 + 8 * s, ph ^ 1u);
         tc_after();
-        const uint32_t col = tmem + lane_off + a_col0 + s * 64u;
-        tmem_st32(col, hi);
-        tmem_st32(col + 32u, lo);
+        const uint32_t col = tmem + lane_off + a_col0 + s * 64u + (uint32_t)hf * 16u;
+        tmem_st16(col, hi);
+        tmem_st16(col + 32u, lo);
         tmem_wait_st();
         tc_before();
         mbar_arrive(full0 + 8 * s);
@@ -394,6 +400,19 @@ __global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, in
   }
 }
 
+// im2col tap table in the reference's (k,i,j) order; padding entries (k >= K) carry
+// validity bits 15/31 that no pixel mask has, so they load nothing.
+__global__ void k_build_tab(int2* tab, int C, int H, int R, int K, int Kpad) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Kpad) return;
+  if (k >= K) {
+    tab[k] = make_int2(0, (int)0x80008000u);
+    return;
+  }
+  const int RR = R * R, c = k / RR, t = k % RR, i = t / R, j = t % R;
+  tab[k] = make_int2((c * H + i) * H + j, (int)((1u << i) | (1u << (16 + j))));
+}
+
 int g_num_sms = 0;
 
 template <int BN>
@@ -401,7 +420,7 @@ int launch_bn(const TcArgs& a, int grid, size_t smem, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(1024 + kStages * BN * 256 + 256)));
+                                        227 * 1024));
     attr_set = true;
   }
   FTC_LAUNCH(k_conv_tc<BN><<<grid, kThreads, smem, s>>>(a));
@@ -413,6 +432,12 @@ int launch_bn(const TcArgs& a, int grid, size_t smem, cudaStream_t s) {
 
 bool tc_supported(const ftc_conv_desc& d) {
   if (d.groups != 1) return false;
+  if (d.R > 15) return false;  // tap validity bits: rows 0-14, columns 16-30
+  const long long K = (long long)d.C * d.R * d.R;
+  const long long nkc = (K + kBK - 1) / kBK;
+  const long long bn = d.M <= 128 ? ((d.M + 31) / 32) * 32 : 128;
+  if (1024 + kStages * bn * 256 + nkc * kBK * 8 + 256 > 227 * 1024) return false;
+  if ((long long)d.C * d.H * d.H >= (1LL << 31)) return false;
   const long long E = (d.H + 2LL * d.pad - d.R) / d.stride + 1;
   if ((long long)d.N * E * E >= (1LL << 31)) return false;
   return true;
@@ -438,6 +463,14 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
     return FTC_CUDA_ERROR;
   }
   FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, d.M, p->K, p->BN, p->ntiles, p->nkc));
+  if (cudaMalloc(&p->tab, (size_t)p->nkc * kBK * sizeof(int2)) != cudaSuccess) {
+    cudaFree(p->Wp);
+    delete p;
+    set_error(FTC_CUDA_ERROR, "cudaMalloc(tap table) failed");
+    return FTC_CUDA_ERROR;
+  }
+  FTC_LAUNCH(k_build_tab<<<(p->nkc * kBK + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->K,
+                                                                   p->nkc * kBK));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFree(p->Wp);
@@ -452,6 +485,7 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
 void tc_plan_destroy(TcPlan* p) {
   if (!p) return;
   if (p->Wp) cudaFree(p->Wp);
+  if (p->tab) cudaFree(p->tab);
   delete p;
 }
 
@@ -461,6 +495,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   TcArgs a{};
   a.D = c.D;
   a.Wp = p->Wp;
+  a.tab = p->tab;
   a.bias = c.bias;
   a.O = c.O;
   a.N = c.N;
@@ -495,7 +530,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   }
   const int tiles = a.ntiles * a.npt;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  const size_t smem = 1024 + (size_t)kStages * p->BN * 256 + 256;
+  const size_t smem = 1024 + (size_t)kStages * p->BN * 256 + (size_t)p->nkc * kBK * 8 + 256;
   switch (p->BN) {
     case 32: return launch_bn<32>(a, grid, smem, s);
     case 64: return launch_bn<64>(a, grid, smem, s);

@@ -1,0 +1,422 @@
+"""BASELINE conv stacks (configs 2-5) as protected-layer pipelines on one GPU (or one
+shard per rank).
+
+Each net is a list of ops over named activations:
+    Conv(src, dst, M, R, stride, pad, bias)  -- an ABFT-protected layer (ProtectedConv)
+    ActPool(src, dst, act, k, s, p)          -- act then max pool (k=1: activation only)
+    AddAct(a, b, dst, act)                   -- residual add + activation
+    PadCrop(src, dst, lo, hi)                -- explicit pad/crop for floor-mode strides
+The reference chains protected convs directly and has no glue ops (replay.hpp:14-25);
+the glue here is a harness-side extension and runs in CUDA (ftc_glue.cu).
+
+Execution is optimistic: every layer's clean path (checksums, conv, fused sums,
+CoC-D) is enqueued back to back; verdicts are collected afterwards.  If a layer
+reports a repair (coc/rc/clc/fc/recompute), its downstream layers -- which consumed
+the unrepaired output -- are re-run.  Inputs are seeded synthetic tensors
+(SURVEY 8(d)); weights are He-normal; ResNet's BN is folded into W and a bias.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi, synth
+from .ftconv import ConvParams, LayerPlan, ProtectedConv, _check
+
+ACT = {"none": 0, "relu": 1, "leaky": 2}
+
+
+@dataclass
+class Conv:
+    src: str
+    dst: str
+    M: int
+    R: int
+    stride: int = 1
+    pad: int = 0
+    bias: bool = False
+
+
+@dataclass
+class ActPool:
+    src: str
+    dst: str
+    act: str = "relu"
+    k: int = 1
+    s: int = 1
+    p: int = 0
+
+
+@dataclass
+class AddAct:
+    a: str
+    b: str
+    dst: str
+    act: str = "relu"
+
+
+@dataclass
+class PadCrop:
+    src: str
+    dst: str
+    lo: int
+    hi: int
+
+
+# ----------------------------------------------------------------------------- definitions
+def alexnet():
+    """BASELINE configs[1]: AlexNet-style 5-layer stack, batch 128, input 3x227x227 N(0,1)."""
+    return dict(name="alexnet", batch=128, C=3, H=227, input="normal", ops=[
+        Conv("x", "c1", 96, 11, 4, 0), ActPool("c1", "p1", "relu", 3, 2),
+        Conv("p1", "c2", 256, 5, 1, 2), ActPool("c2", "p2", "relu", 3, 2),
+        Conv("p2", "c3", 384, 3, 1, 1), ActPool("c3", "a3", "relu"),
+        Conv("a3", "c4", 384, 3, 1, 1), ActPool("c4", "a4", "relu"),
+        Conv("a4", "c5", 256, 3, 1, 1), ActPool("c5", "out", "relu", 3, 2),
+    ])
+
+
+def vgg19():
+    """BASELINE configs[2]: VGG-19 conv trunk, batch 64, 3x224x224 N(0,1)."""
+    ops, src, i = [], "x", 0
+    blocks = [[64, 64], [128, 128], [256] * 4, [512] * 4, [512] * 4]
+    for b, widths in enumerate(blocks):
+        for w in widths:
+            i += 1
+            ops.append(Conv(src, f"c{i}", w, 3, 1, 1))
+            ops.append(ActPool(f"c{i}", f"a{i}", "relu"))
+            src = f"a{i}"
+        if b < len(blocks) - 1:
+            ops.append(ActPool(src, f"pool{b}", "none", 2, 2))
+            src = f"pool{b}"
+    ops[-1].dst = "out"
+    return dict(name="vgg19", batch=64, C=3, H=224, input="normal", ops=ops)
+
+
+def resnet18():
+    """BASELINE configs[3]: ResNet-18 convs, batch 256, BN folded (scale U(0.5,1.5), bias
+    U(-0.1,0.1)).  Stride-2 convs go through explicit pad/crop so the reference's exact
+    extent rule holds; maxpool 3x3 s2 uses pad 1 (torchvision)."""
+    ops = [PadCrop("x", "xp", 3, 2), Conv("xp", "stem", 64, 7, 2, 0, True),
+           ActPool("stem", "s0", "relu", 3, 2, 1)]
+    src, width, H = "s0", 64, 56
+    k = 0
+    for stage, w in enumerate([64, 128, 256, 512]):
+        for blk in range(2):
+            k += 1
+            down = stage > 0 and blk == 0
+            t = f"b{k}"
+            if down:
+                ops.append(PadCrop(src, f"{t}_pad", 1, 0))
+                ops.append(Conv(f"{t}_pad", f"{t}_c1", w, 3, 2, 0, True))
+                ops.append(PadCrop(src, f"{t}_crop", 0, -1))
+                ops.append(Conv(f"{t}_crop", f"{t}_proj", w, 1, 2, 0, True))
+                shortcut = f"{t}_proj"
+            else:
+                ops.append(Conv(src, f"{t}_c1", w, 3, 1, 1, True))
+                shortcut = src
+            ops.append(ActPool(f"{t}_c1", f"{t}_a1", "relu"))
+            ops.append(Conv(f"{t}_a1", f"{t}_c2", w, 3, 1, 1, True))
+            ops.append(AddAct(f"{t}_c2", shortcut, f"{t}_out", "relu"))
+            src = f"{t}_out"
+    ops[-1].dst = "out"
+    return dict(name="resnet18", batch=256, C=3, H=224, input="normal", ops=ops, bn_fold=True)
+
+
+def yolov2():
+    """BASELINE configs[4]: YOLOv2/Darknet-19-style convs (18 backbone + 3 head = 21),
+    batch 64, 3x416x416 U(0,1), leaky-ReLU 0.1, maxpool 2x2 s2 between groups."""
+    groups = [[(32, 3)], [(64, 3)], [(128, 3), (64, 1), (128, 3)], [(256, 3), (128, 1), (256, 3)],
+              [(512, 3), (256, 1), (512, 3), (256, 1), (512, 3)],
+              [(1024, 3), (512, 1), (1024, 3), (512, 1), (1024, 3)]]
+    ops, src, i = [], "x", 0
+    for g, layers in enumerate(groups):
+        for (w, r) in layers:
+            i += 1
+            ops.append(Conv(src, f"c{i}", w, r, 1, r // 2))
+            ops.append(ActPool(f"c{i}", f"a{i}", "leaky"))
+            src = f"a{i}"
+        if g < len(groups) - 1:
+            ops.append(ActPool(src, f"pool{g}", "none", 2, 2))
+            src = f"pool{g}"
+    for (w, r, act) in [(1024, 3, "leaky"), (1024, 3, "leaky"), (425, 1, None)]:
+        i += 1
+        ops.append(Conv(src, f"c{i}", w, r, 1, r // 2))
+        if act:
+            ops.append(ActPool(f"c{i}", f"a{i}", act))
+            src = f"a{i}"
+        else:
+            src = f"c{i}"
+    return dict(name="yolov2", batch=64, C=3, H=416, input="uniform", ops=ops, output=src)
+
+
+NETS = {"alexnet": alexnet, "vgg19": vgg19, "resnet18": resnet18, "yolov2": yolov2}
+
+
+def shapes(net):
+    """Propagate (C, H) through the op list; returns {tensor: (C, H)} and conv dims."""
+    sh = {"x": (net["C"], net["H"])}
+    convs = []
+    for op in net["ops"]:
+        if isinstance(op, Conv):
+            Cin, H = sh[op.src]
+            if (H + 2 * op.pad - op.R) % op.stride:
+                raise ValueError(f"{op.dst}: extent not integral")
+            E = (H + 2 * op.pad - op.R) // op.stride + 1
+            sh[op.dst] = (op.M, E)
+            convs.append((op, Cin, H, E))
+        elif isinstance(op, ActPool):
+            Cin, H = sh[op.src]
+            sh[op.dst] = (Cin, (H + 2 * op.p - op.k) // op.s + 1)
+        elif isinstance(op, AddAct):
+            sh[op.dst] = sh[op.a]
+        elif isinstance(op, PadCrop):
+            Cin, H = sh[op.src]
+            sh[op.dst] = (Cin, H + op.lo + op.hi)
+    return sh, convs
+
+
+def net_weights(net, seed):
+    """He-normal kernels; ResNet: BN folded as W' = s*W, bias b."""
+    _, convs = shapes(net)
+    out = {}
+    for li, (op, Cin, H, E) in enumerate(convs):
+        W = synth.he_normal(op.M, Cin, op.R, seed * 1000 + li)
+        b = None
+        if op.bias:
+            g = np.random.default_rng(seed * 1000 + 500 + li)
+            scale = g.uniform(0.5, 1.5, op.M).astype(np.float32)
+            W = (W * scale[:, None, None, None]).astype(np.float32)
+            b = g.uniform(-0.1, 0.1, op.M).astype(np.float32)
+        out[op.dst] = (W, b)
+    return out
+
+
+def net_input(net, batch, seed):
+    shape = (batch, net["C"], net["H"], net["H"])
+    if net["input"] == "uniform":
+        return synth.uniform(shape, 0.0, 1.0, seed)
+    return synth.normal(shape, 1.0, seed)
+
+
+# ----------------------------------------------------------------------------- GPU runner
+class ProtectedNet:
+    """All layers of one net on one device (one data-parallel shard)."""
+
+    def __init__(self, net, batch: int, seed: int, dev, taus=None, rc=True, clc=True):
+        import torch
+        self.net, self.batch, self.dev = net, batch, dev
+        self.torch = torch
+        self.sh, self.convs = shapes(net)
+        self.weights = net_weights(net, seed)
+        self.layers = {}
+        self.plans = {}
+        for op, Cin, H, E in self.convs:
+            W, b = self.weights[op.dst]
+            p = ConvParams(stride=op.stride, pad=op.pad, bias_enabled=op.bias)
+            self.layers[op.dst] = ProtectedConv(W, b, p, batch, H)
+            tau = (taus or {}).get(op.dst, 1e-3)
+            self.plans[op.dst] = LayerPlan(rc_enabled=rc, clc_enabled=clc, tau=tau)
+        self.buf = {}
+        for name, (c, h) in self.sh.items():
+            self.buf[name] = torch.empty((batch, c, h, h), dtype=torch.float32, device=dev)
+        self.out_name = net.get("output", "out")
+        self.flops = sum(2.0 * batch * op.M * E * E * Cin * op.R * op.R for op, Cin, H, E in self.convs)
+
+    def set_input(self, x):
+        self.buf["x"].copy_(x if not isinstance(x, np.ndarray) else self.torch.from_numpy(x))
+
+    def _glue(self, op, stream):
+        L = _abi.lib()
+        s = stream.cuda_stream
+        if isinstance(op, ActPool):
+            c, h = self.sh[op.src]
+            _check(L.ftc_glue_act_pool(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), self.batch,
+                                       c, h, ACT[op.act], op.k, op.s, op.p, None, s), "act_pool")
+        elif isinstance(op, AddAct):
+            _check(L.ftc_glue_add_act(self.buf[op.a].data_ptr(), self.buf[op.b].data_ptr(),
+                                      self.buf[op.dst].data_ptr(), self.buf[op.a].numel(), ACT[op.act], s),
+                   "add_act")
+        elif isinstance(op, PadCrop):
+            c, h = self.sh[op.src]
+            _check(L.ftc_glue_pad_crop(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), self.batch,
+                                       c, h, op.lo, op.hi, s), "pad_crop")
+
+    def _ops_from(self, start: int, stream, protected: bool, faults=None, sync_each=False):
+        reps = {}
+        for op in self.net["ops"][start:]:
+            if isinstance(op, Conv):
+                L = self.layers[op.dst]
+                if protected:
+                    L.launch(self.buf[op.src], self.buf[op.dst], self.plans[op.dst],
+                             (faults or {}).get(op.dst, ()), stream)
+                    if sync_each:
+                        reps[op.dst] = L.finish()
+                else:
+                    L.conv_forward(self.buf[op.src], self.buf[op.dst], stream)
+            else:
+                self._glue(op, stream)
+        return reps
+
+    def launch(self, faults=None, stream=None):
+        """Enqueue the clean path of every layer (no host synchronisation)."""
+        stream = stream or self.torch.cuda.current_stream()
+        self._pending_faults = faults
+        self._ops_from(0, stream, True, faults)
+
+    def finish(self, stream=None):
+        """Collect verdicts in layer order; re-run downstream layers after a repair."""
+        stream = stream or self.torch.cuda.current_stream()
+        reps = {}
+        ops = self.net["ops"]
+        idx = 0
+        while idx < len(ops):
+            op = ops[idx]
+            idx += 1
+            if not isinstance(op, Conv):
+                continue
+            rep = self.layers[op.dst].finish()
+            rep.layer = op.dst
+            reps[op.dst] = rep
+            if rep.stage in ("coc", "rc", "clc", "fc", "recompute") and idx < len(ops):
+                # downstream consumed the unrepaired output: finish the stale in-flight
+                # layers, then replay from here with the faults already spent
+                for op2 in ops[idx:]:
+                    if isinstance(op2, Conv):
+                        self.layers[op2.dst].finish()
+                self._ops_from(idx, stream, True, None)
+        return reps
+
+    def forward(self, faults=None, stream=None):
+        self.launch(faults, stream)
+        return self.finish(stream)
+
+    def unprotected(self, stream=None):
+        self._ops_from(0, stream or self.torch.cuda.current_stream(), False)
+
+    def output(self):
+        return self.buf[self.out_name]
+
+    def close(self):
+        for L in self.layers.values():
+            L.close()
+
+
+def calibrate_taus(net, batch, seed, dev, factor=4.0):
+    """tau_L per layer: >= 4x the max fault-free FP64 residual over all
+    seven families of the FP32 output, rounded up to a power of ten."""
+    import torch
+    from .ftconv import input_checksums, output_checksums, output_summations
+    pn = ProtectedNet(net, batch, seed, dev)
+    pn.set_input(torch.from_numpy(net_input(net, batch, seed)).to(dev))
+    pn.unprotected()
+    taus = {}
+    for op, Cin, H, E in pn.convs:
+        L = pn.layers[op.dst]
+        W = torch.from_numpy(pn.weights[op.dst][0]).to(dev)
+        b = pn.weights[op.dst][1]
+        D = pn.buf[op.src]
+        ic = input_checksums(D, W, 1)
+        cs = output_checksums(127, D, W, ic, L.p)
+        so = output_summations(pn.buf[op.dst], 127, torch.from_numpy(b).to(dev) if b is not None else None)
+        worst = 0.0
+        for c, s in zip(cs, so):
+            den = torch.clamp(torch.maximum(c.abs(), s.abs()), min=1.0)
+            worst = max(worst, float(((c - s).abs() / den).max()))
+        taus[op.dst] = 10.0 ** math.ceil(math.log10(max(worst * factor, 1e-7)))
+    torch.cuda.synchronize()
+    pn.close()
+    return taus
+
+
+class BenchNet:
+    """bench.py adapter: protected forward of one shard, unprotected forward, e2e."""
+
+    def __init__(self, name, seed, dev):
+        import torch
+        net = NETS[name]()
+        self.net = net
+        self.batch = net["batch"]
+        self.taus = calibrate_taus(net, self.batch, 11, dev)
+        self.pn = ProtectedNet(net, self.batch, 11, dev, self.taus)
+        x = net_input(net, self.batch, seed)
+        self.x_host = torch.from_numpy(x).pin_memory()
+        self.pn.set_input(self.x_host.to(dev))
+        self.layers = list(self.pn.layers.values())
+        self.flops = self.pn.flops
+        out = self.pn.output()
+        self.out_host = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        self.in_bytes = x.nbytes
+        self.out_bytes = self.out_host.numel() * 4
+
+    def launch(self):
+        self.pn.launch()
+
+    def finish(self):
+        return list(self.pn.finish().values())
+
+    def unprotected(self):
+        self.pn.unprotected()
+
+    def e2e(self):
+        # the public entry a user calls: host batch in, protected forward, host result out
+        self.pn.buf["x"].copy_(self.x_host, non_blocking=True)
+        reps = self.pn.forward()
+        self.out_host.copy_(self.pn.output(), non_blocking=True)
+        self.pn.torch.cuda.current_stream().synchronize()
+        return list(reps.values())
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def _np_act_pool(x, act, k, s, p):
+    if act == "relu":
+        x = np.maximum(x, 0)
+    elif act == "leaky":
+        x = np.where(x > 0, x, np.float32(0.1) * x)
+    if k == 1 and s == 1 and p == 0:
+        return x.astype(np.float32)
+    N, Cc, H, _ = x.shape
+    Ho = (H + 2 * p - k) // s + 1
+    xp = np.full((N, Cc, H + 2 * p, H + 2 * p), -np.inf, np.float32)
+    xp[:, :, p:p + H, p:p + H] = x
+    out = np.full((N, Cc, Ho, Ho), -np.inf, np.float32)
+    for i in range(k):
+        for j in range(k):
+            out = np.maximum(out, xp[:, :, i:i + s * Ho:s, j:j + s * Ho:s][:, :, :Ho, :Ho])
+    return out
+
+
+def reference_forward(name, seed, images):
+    """The reference's shipped CPU path through the whole net on `images` images:
+    run_protected_layer<float> (make_default_plan, tau 1e-4, ConvImpl::direct) per
+    conv via oracle/_ref, numpy glue in between.  Used for bench.py's CPU baseline."""
+    import os
+    import sys
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(here, "oracle"))
+    import oracle_py as O
+    net = NETS[name]()
+    sh, convs = shapes(net)
+    wts = net_weights(net, 11)
+    t = {"x": net_input(net, images, seed)}
+    for op in net["ops"]:
+        if isinstance(op, Conv):
+            W, b = wts[op.dst]
+            Cin, H = sh[op.src]
+            d = O.dims(images, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias)
+            _, t[op.dst] = O.ref_protected_layer_f32(d, t[op.src], W, b, tau=1e-4)
+        elif isinstance(op, ActPool):
+            t[op.dst] = _np_act_pool(t[op.src], op.act, op.k, op.s, op.p)
+        elif isinstance(op, AddAct):
+            t[op.dst] = _np_act_pool(t[op.a] + t[op.b], op.act, 1, 1, 0)
+        elif isinstance(op, PadCrop):
+            x = t[op.src]
+            H = x.shape[2]
+            Ho = H + op.lo + op.hi
+            y = np.zeros(x.shape[:2] + (Ho, Ho), np.float32)
+            src = x[:, :, :min(H, Ho - op.lo), :min(H, Ho - op.lo)]
+            y[:, :, op.lo:op.lo + src.shape[2], op.lo:op.lo + src.shape[3]] = src
+            t[op.dst] = y
+    return t
