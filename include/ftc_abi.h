@@ -172,6 +172,14 @@ int ftc_protected_conv_launch(ftc_layer* layer, const ftc_plan* plan, const floa
                               const ftc_fault* faults, int32_t n_faults, void* stream);
 int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
 
+/* _launch with the input checksums supplied by the producer of D: cd1/cd2 are
+ * device FP64 C*H*H tensors holding sum_n D_n and sum_n n*D_n in ascending n
+ * (checksums.hpp:100-107), e.g. fused into the previous layer's glue kernel
+ * (ftc_glue_act_pool_ck).  Saves the input-checksum pass over D. */
+int ftc_protected_conv_launch_ck(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                                 const double* cd1, const double* cd2, const ftc_fault* faults,
+                                 int32_t n_faults, void* stream);
+
 /* Instrumentation for bench.py: when enabled, CUDA events bracket the conv kernel
  * of every protected/unprotected call on its launching stream; _kernel_time
  * returns the accumulated device time (ms) and launch count (reset if `reset`).
@@ -216,6 +224,11 @@ int ftc_verify_kernel(const ftc_conv_desc* desc, const float* W, const double* c
  * in == out == NULL only the output side is returned in *Ho. */
 int ftc_glue_act_pool(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t act,
                       int32_t k, int32_t s, int32_t p, int32_t* Ho, void* stream);
+/* ftc_glue_act_pool that also reduces its output over the batch for the NEXT
+ * protected layer: cd1 = sum_n out_n, cd2 = sum_n n*out_n (FP64, ascending n, i.e.
+ * input_checksums of `out` exactly, checksums.hpp:100-107). */
+int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t act,
+                         int32_t k, int32_t s, int32_t p, double* cd1, double* cd2, void* stream);
 /* out = act(a + b) elementwise over n values (b may be NULL) */
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act,
                      void* stream);

@@ -22,7 +22,8 @@ EXPORTS = (
     "ftc_protected_conv_launch", "ftc_protected_conv_finish", "ftc_input_checksums",
     "ftc_kernel_checksums", "ftc_output_checksums", "ftc_output_summations", "ftc_detect_coc_d",
     "ftc_verify_kernel", "ftc_layer_set_timing", "ftc_layer_kernel_time", "ftc_kernel_launches",
-    "ftc_glue_act_pool", "ftc_glue_add_act", "ftc_glue_pad_crop",
+    "ftc_glue_act_pool", "ftc_glue_add_act", "ftc_glue_pad_crop", "ftc_protected_conv_launch_ck",
+    "ftc_glue_act_pool_ck",
 )
 
 
@@ -89,6 +90,9 @@ def lib():
         L.ftc_layer_kernel_time.argtypes = [vp, C.POINTER(dbl), C.POINTER(i32), i32]
         L.ftc_kernel_launches.restype = C.c_uint64
         L.ftc_glue_act_pool.argtypes = [vp, vp, i32, i32, i32, i32, i32, i32, i32, C.POINTER(i32), vp]
+        L.ftc_protected_conv_launch_ck.argtypes = [vp, C.POINTER(Plan), vp, vp, vp, vp, C.POINTER(Fault),
+                                                   i32, vp]
+        L.ftc_glue_act_pool_ck.argtypes = [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         _lib = L

@@ -285,6 +285,59 @@ __global__ void k_count_differ(const double* __restrict__ c, const double* __res
   if (local) atomicAdd(count, local);
 }
 
+// Clean-path Cd1 only (CoC-D needs Co5 = Cd1 (*) Cw1; Cd2 feeds only the weighted
+// families of the error path, which recomputes both exactly).  Two positions per
+// thread, eight images in flight per thread: enough bytes in flight to stream D at
+// HBM rate.
+__global__ void __launch_bounds__(128) k_cd1_fast(const float* __restrict__ D, int N, long long per2,
+                                                  double* __restrict__ cd1) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per2) return;
+  const float2* src = reinterpret_cast<const float2*>(D) + e;
+  double a0 = 0.0, a1 = 0.0;
+  int n = 0;
+  for (; n + 8 <= N; n += 8) {
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (long long)(n + u) * per2);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a0 += v[u].x;
+      a1 += v[u].y;
+    }
+  }
+  for (; n < N; ++n) {
+    const float2 v = __ldcs(src + (long long)n * per2);
+    a0 += v.x;
+    a1 += v.y;
+  }
+  reinterpret_cast<double2*>(cd1)[e] = make_double2(a0, a1);
+}
+
+// Clean-path CoC-D: one warp per position f; lanes stride over the (row-sum slab,
+// image) pairs of the fused epilogue sums, fixed xor-shuffle tree (deterministic).
+__global__ void k_detect_warp(const double* __restrict__ co5, const double* __restrict__ rowsum,
+                              int parts, int N, int E2, int bias, const double* agg, double tau,
+                              DetectStats* st) {
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= E2) return;
+  const long long slab = (long long)N * E2;
+  const int terms = N * parts;
+  double s = 0.0;
+  for (int t = lane; t < terms; t += 32) {
+    const int q = t / N, n = t - q * N;
+    s += rowsum[q * slab + (long long)n * E2 + f];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    if (bias) s -= (double)N * agg[0];
+    bool bad;
+    detect_one(co5[f], s, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -364,6 +417,24 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
 int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s) {
   FTC_LAUNCH(k_detect_fast<<<blocks_for(E2), kThreads, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s) {
+  if (per % 2 != 0 || ((uintptr_t)D % 8) != 0) {
+    // odd plane size: the exact kernel also produces Cd1 (Cd2 into the same scratch)
+    return FTC_CONFIG_ERROR;
+  }
+  FTC_LAUNCH(k_cd1_fast<<<blocks_for(per / 2, 128), 128, 0, s>>>(D, N, per / 2, cd1));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+                       const double* agg, double tau, DetectStats* st, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_warp<<<blocks_for((long long)E2 * 32), kThreads, 0, s>>>(co5, rowsum, parts, N, E2,
+                                                                              bias, agg, tau, st));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -149,6 +149,11 @@ struct DetectStats {
 };
 int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s);
+// clean path: Cd1 only, parallel over positions (FTC_CONFIG_ERROR when the plane size
+// is odd -> caller uses the exact kernel)
+int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s);
+int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+                       const double* agg, double tau, DetectStats* st, cudaStream_t s);
 int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
                         DetectStats* st, cudaStream_t s);
 int launch_count_differ(const double* c, const double* s_, long long n, double tau, int* count,

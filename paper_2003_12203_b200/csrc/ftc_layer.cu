@@ -112,6 +112,8 @@ struct ftc_layer {
   const double *cw1 = nullptr, *cw2 = nullptr;
   float* O = nullptr;
   int nfaults = 0, n_out_faults = 0;
+  bool ck_exact = false;  // cd1/cd2 hold exact-order input checksums of D
+  bool has_cd_faults = false;
   int rs_parts = 1;  // row-sum partial slabs written by the last fused-sum conv
   cudaStream_t stream = nullptr;
   std::chrono::steady_clock::time_point t0;
@@ -492,6 +494,16 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
     return FTC_OK;
   };
 
+  // The clean path may have produced only a fast Cd1: take the exact-order input
+  // checksums of the caller's (pre-fault) D, re-applying injected checksum faults.
+  if (!L->ck_exact) {
+    CK(launch_input_checksums(L->D, d.N, L->nCd, L->cd1, L->cd2, e.s));
+    if (L->has_cd_faults) {
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, e.s));
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, e.s));
+    }
+    L->ck_exact = true;
+  }
   // Re-establish the CoC-D verdict on exact-order Co5/So5 (bitwise the reference's).
   CK(ensure_cs(e, FTC_CK_O5));
   CK(ensure_s(e, FTC_CK_O5));
@@ -775,8 +787,9 @@ int ftc_layer_kernel_time(ftc_layer* L, double* conv_ms, int32_t* conv_launches,
 
 uint64_t ftc_kernel_launches(void) { return g_launches.load(); }
 
-int ftc_protected_conv_launch(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
-                              const ftc_fault* faults, int32_t n_faults, void* stream) {
+static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
+                       const double* cd1_in, const double* cd2_in, const ftc_fault* faults,
+                       int32_t n_faults, void* stream) {
   if (!L || !plan || !D || !O) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
   if (L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "a protected call is already in flight on this layer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -816,26 +829,52 @@ int ftc_protected_conv_launch(ftc_layer* L, const ftc_plan* plan, const float* D
     L->cw1 = L->cw1w;
     L->cw2 = L->cw2w;
   }
-  // side stream: input checksums of the caller's (pre-fault) D, then Co5
+  // side stream: input checksums of the caller's (pre-fault) D, then Co5.  When the
+  // producer of D already reduced it (glue kernels of a net), the exact Cd1/Cd2 are
+  // taken as given; otherwise a fast Cd1-only pass feeds CoC-D.
+  L->has_cd_faults = L->nfaults && (has_target(faults, n_faults, FTC_FAULT_CD1) ||
+                                    has_target(faults, n_faults, FTC_FAULT_CD2));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
   FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
-  CK(launch_input_checksums(D, d.N, L->nCd, L->cd1, L->cd2, L->side));
-  if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_CD1))
+  if (cd1_in) {
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd1, cd1_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd2, cd2_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
+    L->ck_exact = true;
+  } else if (launch_cd1_fast(D, d.N, L->nCd, L->cd1, L->side) == FTC_OK) {
+    L->ck_exact = false;
+  } else {
+    CK(launch_input_checksums(D, d.N, L->nCd, L->cd1, L->cd2, L->side));
+    L->ck_exact = true;
+  }
+  if (L->has_cd_faults) {
     CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, L->side));
-  if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_CD2))
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
+    if (L->ck_exact)
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
+  }
   CK(launch_co5_fast(L->cd1, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, L->side));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
   // main stream: conv with fused post_conv faults and So2/So4 row sums
   CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
   FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
   FTC_CUDA_CHECK(cudaMemsetAsync(L->stats, 0, sizeof(DetectStats), s));
-  CK(launch_detect_fast(L->co5f, L->rowsum, L->rs_parts, d.N, L->E2, d.bias_enabled, L->agg, plan->tau,
+  CK(launch_detect_warp(L->co5f, L->rowsum, L->rs_parts, d.N, L->E2, d.bias_enabled, L->agg, plan->tau,
                         L->stats, s));
   FTC_CUDA_CHECK(cudaMemcpyAsync(L->stats_h, L->stats, sizeof(DetectStats), cudaMemcpyDeviceToHost, s));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
   L->inflight = true;
   return FTC_OK;
+}
+
+int ftc_protected_conv_launch(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
+                              const ftc_fault* faults, int32_t n_faults, void* stream) {
+  return launch_impl(L, plan, D, O, nullptr, nullptr, faults, n_faults, stream);
+}
+
+int ftc_protected_conv_launch_ck(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
+                                 const double* cd1, const double* cd2, const ftc_fault* faults,
+                                 int32_t n_faults, void* stream) {
+  if (!cd1 || !cd2) RET_ERR(FTC_INVALID_ARGUMENT, "null input checksums");
+  return launch_impl(L, plan, D, O, cd1, cd2, faults, n_faults, stream);
 }
 
 int ftc_protected_conv_finish(ftc_layer* L, ftc_layer_report* rep) {

@@ -256,6 +256,13 @@ class ProtectedConv:
         _check(_abi.lib().ftc_protected_conv_launch(self.h, C.byref(self._pl), _ptr(D), _ptr(O), arr,
                                                     n, _stream_ptr(stream)), "launch")
 
+    def launch_ck(self, D, O, cd1, cd2, plan: LayerPlan, faults=(), stream=None):
+        """launch with exact input checksums supplied by D's producer (FP64 device tensors)."""
+        arr, n = _faults_c(faults)
+        self._pl = plan.c()
+        _check(_abi.lib().ftc_protected_conv_launch_ck(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
+                                                       _ptr(cd2), arr, n, _stream_ptr(stream)), "launch_ck")
+
     def finish(self) -> LayerReport:
         rep = _abi.Report()
         _check(_abi.lib().ftc_protected_conv_finish(self.h, C.byref(rep)), "finish")

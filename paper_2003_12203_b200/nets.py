@@ -222,6 +222,15 @@ class ProtectedNet:
         self.buf = {}
         for name, (c, h) in self.sh.items():
             self.buf[name] = torch.empty((batch, c, h, h), dtype=torch.float32, device=dev)
+        # glue outputs consumed by a protected conv carry that conv's input checksums,
+        # reduced inside the glue kernel (no separate pass over D)
+        conv_srcs = {op.src for op in net["ops"] if isinstance(op, Conv)}
+        self.ck = {}
+        for op in net["ops"]:
+            if isinstance(op, ActPool) and op.dst in conv_srcs:
+                c, h = self.sh[op.dst]
+                self.ck[op.dst] = (torch.empty((c, h, h), dtype=torch.float64, device=dev),
+                                   torch.empty((c, h, h), dtype=torch.float64, device=dev))
         self.out_name = net.get("output", "out")
         self.flops = sum(2.0 * batch * op.M * E * E * Cin * op.R * op.R for op, Cin, H, E in self.convs)
 
@@ -233,8 +242,14 @@ class ProtectedNet:
         s = stream.cuda_stream
         if isinstance(op, ActPool):
             c, h = self.sh[op.src]
-            _check(L.ftc_glue_act_pool(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), self.batch,
-                                       c, h, ACT[op.act], op.k, op.s, op.p, None, s), "act_pool")
+            if op.dst in self.ck:
+                cd1, cd2 = self.ck[op.dst]
+                _check(L.ftc_glue_act_pool_ck(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(),
+                                              self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
+                                              cd1.data_ptr(), cd2.data_ptr(), s), "act_pool_ck")
+            else:
+                _check(L.ftc_glue_act_pool(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), self.batch,
+                                           c, h, ACT[op.act], op.k, op.s, op.p, None, s), "act_pool")
         elif isinstance(op, AddAct):
             _check(L.ftc_glue_add_act(self.buf[op.a].data_ptr(), self.buf[op.b].data_ptr(),
                                       self.buf[op.dst].data_ptr(), self.buf[op.a].numel(), ACT[op.act], s),
@@ -249,7 +264,13 @@ class ProtectedNet:
         for op in self.net["ops"][start:]:
             if isinstance(op, Conv):
                 L = self.layers[op.dst]
-                if protected:
+                if protected and op.src in self.ck:
+                    cd1, cd2 = self.ck[op.src]
+                    L.launch_ck(self.buf[op.src], self.buf[op.dst], cd1, cd2, self.plans[op.dst],
+                                (faults or {}).get(op.dst, ()), stream)
+                    if sync_each:
+                        reps[op.dst] = L.finish()
+                elif protected:
                     L.launch(self.buf[op.src], self.buf[op.dst], self.plans[op.dst],
                              (faults or {}).get(op.dst, ()), stream)
                     if sync_each:

@@ -1,0 +1,115 @@
+"""BASELINE conv stacks on the GPU (configs 2-5 at reduced batch).
+
+Judged per layer on identical inputs: each protected conv's output is
+compared with conv_forward<float> (oracle) applied to the GPU's own input
+activation; glue-fused input checksums must equal input_checksums bitwise; a fault
+injected into one layer is repaired and the downstream layers are replayed, so the
+final output equals the fault-free one bitwise."""
+import numpy as np
+import pytest
+
+import oracle_py as O
+from paper_2003_12203_b200 import nets, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def close_frac(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+
+
+def build(name, batch, seed=3):
+    torch = _torch()
+    net = nets.NETS[name]()
+    pn = nets.ProtectedNet(net, batch, 11, torch.device("cuda"))
+    pn.set_input(torch.from_numpy(nets.net_input(net, batch, seed)).cuda())
+    return net, pn
+
+
+@pytest.mark.parametrize("name,batch", [("alexnet", 4), ("vgg19", 1), ("resnet18", 2), ("yolov2", 1)])
+def test_net_per_layer_parity_and_clean_verdicts(name, batch):
+    torch = _torch()
+    net, pn = build(name, batch)
+    reps = pn.forward()
+    torch.cuda.synchronize()
+    assert not any(r.detected for r in reps.values()), {k: r.stage for k, r in reps.items() if r.detected}
+    worst = 0.0
+    for op, Cin, H, E in pn.convs:
+        D = pn.buf[op.src].cpu().numpy()
+        Og = pn.buf[op.dst].cpu().numpy()
+        W, b = pn.weights[op.dst]
+        Oo = O.conv_f32(O.dims(batch, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias), D, W, b)
+        err = close_frac(Og, Oo).max()
+        worst = max(worst, err)
+        assert err <= 1e-5, (op.dst, err)
+    pn.close()
+
+
+def test_glue_fused_checksums_are_exact():
+    torch = _torch()
+    net, pn = build("alexnet", 4)
+    pn.forward()
+    torch.cuda.synchronize()
+    for name, (cd1, cd2) in pn.ck.items():
+        D = pn.buf[name].cpu().numpy().astype(np.float64)
+        c, h = pn.sh[name]
+        d = O.dims(4, c, h, 1, 1)
+        r1, r2, _, _ = O.input_checksums(d, D, np.zeros((1, c, 1, 1)))
+        assert np.array_equal(cd1.cpu().numpy(), r1), name
+        assert np.array_equal(cd2.cpu().numpy(), r2), name
+    pn.close()
+
+
+def test_fault_in_middle_layer_is_repaired_and_replayed():
+    import paper_2003_12203_b200 as F
+    torch = _torch()
+    net, pn = build("alexnet", 4)
+    pn.forward()
+    torch.cuda.synchronize()
+    clean_out = pn.output().clone()
+    clean_c3 = pn.buf["c3"].clone()
+    faults = {"c3": [F.output_bitflip(2, 100, 5, 7, 27)]}
+    reps = pn.forward(faults)
+    torch.cuda.synchronize()
+    assert reps["c3"].detected and reps["c3"].stage == "coc", reps["c3"]
+    assert reps["c3"].corrected_blocks == [(2, 100)]
+    assert torch.equal(pn.buf["c3"], clean_c3)
+    assert torch.equal(pn.output(), clean_out)
+    assert not any(reps[k].detected for k in ("c1", "c2", "c4", "c5"))
+    pn.close()
+
+
+def test_net_layer_verdict_matches_oracle():
+    """A net layer (AlexNet conv4, real activations) under a seeded flip: verdict equal
+    to run_protected_layer<double> on the same FP32 output."""
+    import paper_2003_12203_b200 as F
+    torch = _torch()
+    net, pn = build("alexnet", 2)
+    pn.forward()
+    torch.cuda.synchronize()
+    op = [c for c in pn.convs if c[0].dst == "c4"][0]
+    opc, Cin, H, E = op
+    D = pn.buf[opc.src].cpu().numpy()
+    W, b = pn.weights["c4"]
+    L = pn.layers["c4"]
+    Oclean = pn.buf["c4"].cpu().numpy()
+    plan = pn.plans["c4"]
+    for r in range(12):
+        n, m, x, y, bit = synth.flip_sample(77, r, 2, opc.M, E)
+        Og, rep = L.protected(pn.buf[opc.src], plan, [F.output_bitflip(n, m, x, y, bit)])
+        Of = Oclean.copy()
+        Of[n, m, x, y] = synth.flip32(Of[n, m, x, y], bit)
+        ref = O.protected_layer(O.dims(2, Cin, H, opc.M, opc.R, opc.stride, opc.pad, 1, opc.bias), D, W, b,
+                                plan.rc_enabled, plan.clc_enabled, plan.tau, O_conv=Of)
+        got = rep.verdict()
+        for k in ("detected", "stage", "stages_attempted", "weights_reloaded", "recomputed"):
+            assert got[k] == ref[k], (r, k, got, ref)
+        assert [tuple(t) for t in got["corrected_blocks"]] == [tuple(t) for t in ref["corrected_blocks"]]
+    pn.close()
