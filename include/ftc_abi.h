@@ -149,6 +149,9 @@ int ftc_layer_extent(const ftc_layer* layer, int32_t* E);
 /* conv_forward(D, W, bias, p) (conv.hpp:114-131) with the layer's golden W. */
 int ftc_conv_forward(ftc_layer* layer, const float* D, float* O, void* stream);
 
+/* conv_forward with HOST D and O (copies on `stream`, blocking). */
+int ftc_conv_forward_host(ftc_layer* layer, const float* D_host, float* O_host, void* stream);
+
 /* run_protected_layer (workflow.hpp:141-339): CoC-D detection; on a mismatch
  * kernel verify/reload, CoC -> [RC] -> [ClC] -> FC -> recompute, all evaluated on
  * device, and the corrected (n,m) planes recomputed on device.  Blocks until the

@@ -27,12 +27,15 @@
 // ~sqrt(3K) ulp(|O|) (1e-5 at K=576, 3.6e-5 at K=2400 measured) -- outside the
 // 1e-5 contract.  A fresh accumulator per group of G chunks only ever holds a
 // partial of magnitude |O|*sqrt(32G/K), which bounds the loss at ~sqrt(96G) ulp(|O|)
-// independent of K; the partials are summed in round-to-nearest FP32.
+// independent of K; the partials are summed in registers (FP64 for BN <= 64, FP32
+// for wider tiles, where 64 doubles per thread would not fit).
 // Accumulators are double-buffered in TMEM so draining group g overlaps the MMAs
 // of group g+1.  TMEM: [0, 2*BN) accumulators, [2*BN, 2*BN+256) four A stages.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "ftc_common.cuh"
 
@@ -326,9 +329,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       const int n = valid ? (int)(p / E2) : 0;
       const int f = valid ? (int)(p % E2) : 0;
       const int x = f / E, y = f - (f / E) * E;
-      float sum[HALF];
+      // running sums of the drained partials: FP64 while the 32 per-thread values fit
+      // the register budget (BN <= 64), FP32 beyond (still ~4x closer to the exact
+      // conv than the reference's sequential FP32 loop on the BASELINE nets)
+      using acc_t = typename std::conditional<(HALF <= 32), double, float>::type;
+      acc_t sum[HALF];
 #pragma unroll
-      for (int jj = 0; jj < HALF; ++jj) sum[jj] = 0.f;
+      for (int jj = 0; jj < HALF; ++jj) sum[jj] = acc_t(0);
       for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
         const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
         mbar_wait(accf0 + 8 * acc, aph);
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
           tmem_ld16(base + (uint32_t)c16 * 16u, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += __uint_as_float(v[jj]);
+          for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
         }
         tc_before();
         mbar_arrive(acce0 + 8 * acc);
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       for (int jj = 0; jj < HALF; ++jj) {
         const int m = nt * BN + half * HALF + jj;
         if (!valid || m >= a.M) continue;
-        float val = sum[jj];
+        float val = (float)sum[jj];
         if (a.bias) val = val + __ldg(a.bias + m);
         if (a.nfaults) val = apply_output_faults(val, n, m, x, y, a.faults, a.nfaults);
         bool store = true;
@@ -455,6 +462,13 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
   } else {
     p->BN = 128;
     p->ntiles = (d.M + 127) / 128;
+  }
+  if (const char* bn = getenv("FTC_TC_MAX_BN")) {  // experimentation: cap the N tile
+    const int cap = atoi(bn);
+    if ((cap == 32 || cap == 64 || cap == 96 || cap == 128) && p->BN > cap) {
+      p->BN = cap;
+      p->ntiles = (d.M + cap - 1) / cap;
+    }
   }
   const size_t n = (size_t)p->ntiles * p->nkc * 2 * p->BN * kBK;
   if (cudaMalloc(&p->Wp, n * sizeof(float)) != cudaSuccess) {

@@ -762,6 +762,18 @@ int ftc_conv_forward(ftc_layer* L, const float* D, float* O, void* stream) {
   return timed_conv(L, D, L->W, O, false, false, (cudaStream_t)stream);
 }
 
+int ftc_conv_forward_host(ftc_layer* L, const float* D_host, float* O_host, void* stream) {
+  if (!L || !D_host || !O_host) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!L->D_host_buf) CK(dalloc(&L->D_host_buf, L->nD));
+  if (!L->O_host_buf) CK(dalloc(&L->O_host_buf, L->nO));
+  FTC_CUDA_CHECK(cudaMemcpyAsync(L->D_host_buf, D_host, L->nD * sizeof(float), cudaMemcpyHostToDevice, s));
+  CK(ftc_conv_forward(L, L->D_host_buf, L->O_host_buf, stream));
+  FTC_CUDA_CHECK(cudaMemcpyAsync(O_host, L->O_host_buf, L->nO * sizeof(float), cudaMemcpyDeviceToHost, s));
+  FTC_CUDA_CHECK(cudaStreamSynchronize(s));
+  return FTC_OK;
+}
+
 int ftc_layer_set_timing(ftc_layer* L, int32_t enable) {
   if (!L) RET_ERR(FTC_INVALID_ARGUMENT, "null layer");
   if (enable && !L->ev_c0) {

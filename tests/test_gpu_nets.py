@@ -2,9 +2,12 @@
 
 Judged per layer on identical inputs: each protected conv's output is
 compared with conv_forward<float> (oracle) applied to the GPU's own input
-activation; glue-fused input checksums must equal input_checksums bitwise; a fault
-injected into one layer is repaired and the downstream layers are replayed, so the
-final output equals the fault-free one bitwise."""
+activation.  Gate: |gpu-ref| <= 1e-5*max(1,|gpu|,|ref|); where the reference's own
+sequential FP32 sum is already further than that from the exact (FP64) conv --
+measured 1.4e-5..1.7e-5 on AlexNet conv2-5 activations -- the gate is that the GPU is
+at least as close to the FP64 conv as the reference is.  Glue-fused input checksums
+must equal input_checksums bitwise; an injected fault's verdict matches the oracle,
+and after a repair the replayed downstream output equals the fault-free one."""
 import numpy as np
 import pytest
 
@@ -45,10 +48,15 @@ def test_net_per_layer_parity_and_clean_verdicts(name, batch):
         D = pn.buf[op.src].cpu().numpy()
         Og = pn.buf[op.dst].cpu().numpy()
         W, b = pn.weights[op.dst]
-        Oo = O.conv_f32(O.dims(batch, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias), D, W, b)
+        d = O.dims(batch, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias)
+        Oo = O.conv_f32(d, D, W, b)
         err = close_frac(Og, Oo).max()
         worst = max(worst, err)
-        assert err <= 1e-5, (op.dst, err)
+        if err > 1e-5:
+            O64 = O.conv_f64(d, D.astype(np.float64), W.astype(np.float64),
+                             None if b is None else b.astype(np.float64))
+            e_gpu, e_ref = close_frac(Og, O64).max(), close_frac(Oo, O64).max()
+            assert e_gpu <= e_ref, (op.dst, err, e_gpu, e_ref)
     pn.close()
 
 
@@ -74,15 +82,30 @@ def test_fault_in_middle_layer_is_repaired_and_replayed():
     pn.forward()
     torch.cuda.synchronize()
     clean_out = pn.output().clone()
-    clean_c3 = pn.buf["c3"].clone()
-    faults = {"c3": [F.output_bitflip(2, 100, 5, 7, 27)]}
-    reps = pn.forward(faults)
-    torch.cuda.synchronize()
-    assert reps["c3"].detected and reps["c3"].stage == "coc", reps["c3"]
-    assert reps["c3"].corrected_blocks == [(2, 100)]
-    assert torch.equal(pn.buf["c3"], clean_c3)
-    assert torch.equal(pn.output(), clean_out)
-    assert not any(reps[k].detected for k in ("c1", "c2", "c4", "c5"))
+    clean_c3 = pn.buf["c3"].cpu().numpy()
+    op, Cin, H, E = [c for c in pn.convs if c[0].dst == "c3"][0]
+    D3 = pn.buf[op.src].cpu().numpy()
+    W3, _ = pn.weights["c3"]
+    plan = pn.plans["c3"]
+    repaired = 0
+    for r in range(6):
+        n, m, x, y, bit = synth.flip_sample(4242, r, 4, op.M, E, 24, 29)
+        reps = pn.forward({"c3": [F.output_bitflip(n, m, x, y, bit)]})
+        torch.cuda.synchronize()
+        Of = clean_c3.copy()
+        Of[n, m, x, y] = synth.flip32(Of[n, m, x, y], bit)
+        ref = O.protected_layer(O.dims(4, Cin, H, op.M, op.R, op.stride, op.pad), D3, W3, None,
+                                plan.rc_enabled, plan.clc_enabled, plan.tau, O_conv=Of)
+        got = reps["c3"].verdict()
+        for k in ("detected", "stage", "stages_attempted"):
+            assert got[k] == ref[k], (r, got, ref)
+        assert not any(reps[k].detected for k in ("c1", "c2"))
+        if got["stage"] in ("coc", "rc", "clc", "fc", "recompute"):
+            repaired += 1
+            assert np.array_equal(pn.buf["c3"].cpu().numpy(), clean_c3)
+            assert torch.equal(pn.output(), clean_out)   # downstream replayed
+            assert not any(reps[k].detected for k in ("c4", "c5"))
+    assert repaired >= 3
     pn.close()
 
 
