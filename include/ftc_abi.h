@@ -160,6 +160,13 @@ int ftc_protected_conv(ftc_layer* layer, const ftc_plan* plan, const float* D, f
                        const ftc_fault* faults, int32_t n_faults, ftc_layer_report* report,
                        void* stream);
 
+/* run_protected_layer for an output computed elsewhere: O (device, N x M x E x E)
+ * plays the role of the post_conv hook's output (workflow.hpp:158-160); detection,
+ * the escalation chain and the repair run exactly as in ftc_protected_conv (repair
+ * rewrites the corrected planes of O from D; recompute rewrites all of O). */
+int ftc_protected_check(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                        ftc_layer_report* report, void* stream);
+
 /* Same as ftc_protected_conv with HOST input/output buffers (the reference's own
  * calling convention: run_protected_layer takes and returns host tensors).  The
  * host<->device copies run on `stream`. */

@@ -23,7 +23,7 @@ EXPORTS = (
     "ftc_kernel_checksums", "ftc_output_checksums", "ftc_output_summations", "ftc_detect_coc_d",
     "ftc_verify_kernel", "ftc_layer_set_timing", "ftc_layer_kernel_time", "ftc_kernel_launches",
     "ftc_glue_act_pool", "ftc_glue_add_act", "ftc_glue_pad_crop", "ftc_protected_conv_launch_ck",
-    "ftc_glue_act_pool_ck", "ftc_conv_forward_host",
+    "ftc_glue_act_pool_ck", "ftc_conv_forward_host", "ftc_protected_check",
 )
 
 
@@ -75,6 +75,7 @@ def lib():
         L.ftc_protected_conv.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32,
                                          C.POINTER(Report), vp]
         L.ftc_protected_conv_host.argtypes = L.ftc_protected_conv.argtypes
+        L.ftc_protected_check.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Report), vp]
         L.ftc_protected_conv_launch.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32,
                                                 vp]
         L.ftc_protected_conv_finish.argtypes = [vp, C.POINTER(Report)]

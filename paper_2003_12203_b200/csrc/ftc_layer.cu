@@ -915,6 +915,33 @@ int ftc_protected_conv_finish(ftc_layer* L, ftc_layer_report* rep) {
   return st;
 }
 
+int ftc_protected_check(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
+                        ftc_layer_report* rep, void* stream) {
+  if (!L || !plan || !D || !O || !rep) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "a protected call is already in flight on this layer");
+  cudaStream_t s = (cudaStream_t)stream;
+  L->t0 = std::chrono::steady_clock::now();
+  L->plan = *plan;
+  L->D = D;
+  L->Dconv = D;
+  L->O = O;
+  L->stream = s;
+  L->Wcur = L->W;
+  L->cw1 = L->cw1g;
+  L->cw2 = L->cw2g;
+  L->nfaults = 0;
+  L->n_out_faults = 0;
+  L->has_cd_faults = false;
+  std::memset(rep, 0, sizeof *rep);
+  // exact input checksums; detection is the error path's exact CoC-D
+  CK(launch_input_checksums(D, L->d.N, L->nCd, L->cd1, L->cd2, s));
+  L->ck_exact = true;
+  int st = error_path(L, rep);
+  rep->t_total_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - L->t0).count();
+  return st;
+}
+
 int ftc_protected_conv(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
                        const ftc_fault* faults, int32_t n_faults, ftc_layer_report* rep,
                        void* stream) {

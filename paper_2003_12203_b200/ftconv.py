@@ -250,6 +250,15 @@ class ProtectedConv:
         _check(st, "ftc_protected_conv")
         return O, LayerReport.from_c(rep)
 
+    def check(self, D, O, plan: LayerPlan, stream=None) -> LayerReport:
+        """run_protected_layer on an output O produced elsewhere (post_conv substitution);
+        O is repaired in place."""
+        rep = _abi.Report()
+        pl = plan.c()
+        _check(_abi.lib().ftc_protected_check(self.h, C.byref(pl), _ptr(D), _ptr(O), C.byref(rep),
+                                              _stream_ptr(stream)), "ftc_protected_check")
+        return LayerReport.from_c(rep)
+
     def launch(self, D, O, plan: LayerPlan, faults=(), stream=None):
         arr, n = _faults_c(faults)
         self._pl = plan.c()
