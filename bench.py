@@ -265,7 +265,9 @@ def main():
     for L in wl.layers:
         lib.ftc_layer_set_timing(L.h, 1)
         lib.ftc_layer_kernel_time(L.h, None, None, 1)
+    from paper_2003_12203_b200 import dist as ftc_dist
     reports = []
+    verdict_tables = []
     l0 = lib.ftc_kernel_launches()
     if world > 1:
         dist.barrier()
@@ -283,7 +285,11 @@ def main():
         e0.record(stream)
         wl.launch()
         e1.record(stream)
-        reports.append(wl.finish())
+        reps = wl.finish()
+        reports.append(reps)
+        if world > 1:
+            # per-forward verdict exchange: the only collective of the ABFT path
+            verdict_tables.append(ftc_dist.gather_verdicts(reps, dev))
         e1.synchronize()
         tot += e0.elapsed_time(e1)
     torch.cuda.synchronize()
@@ -309,12 +315,7 @@ def main():
     detected = sum(1 for reps in reports for r in reps if r.detected)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        # verdict exchange: per-shard detection count gathered over NCCL (the only
-        # cross-GPU traffic of the ABFT path)
-        dv = torch.tensor([detected], dtype=torch.int64, device=dev)
-        gathered = [torch.zeros_like(dv) for _ in range(world)]
-        dist.all_gather(gathered, dv)
-        detected = int(sum(int(g.item()) for g in gathered))
+        detected = sum(ftc_dist.summarize(tab)["detected"] for tab in verdict_tables)
     t_prot, t_unprot, t_e2e = tt.tolist()
 
     if rank == 0:

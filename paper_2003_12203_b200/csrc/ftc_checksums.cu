@@ -338,6 +338,54 @@ __global__ void k_detect_warp(const double* __restrict__ co5, const double* __re
   }
 }
 
+// Clean-path CoC-D in one kernel: per position f one warp computes
+//   Co5[f] = conv_block(Cd1, Cw1)[f]   (lanes over input channels, taps unrolled) and
+//   So5[f] = sum over the fused epilogue row sums (lanes over (slab, image) pairs),
+// both reduced with a fixed xor-shuffle tree, then compares them (values_differ).
+__global__ void k_detect_fused(const double* __restrict__ cd1, const double* __restrict__ cw1,
+                               const double* __restrict__ rowsum, int parts, int N, int C, int H,
+                               int R, int U, int pad, int E, int bias, const double* agg,
+                               double tau, DetectStats* st) {
+  const int E2 = E * E;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= E2) return;
+  const int x = f / E, y = f - (f / E) * E;
+  const int hb = x * U - pad, wb = y * U - pad;
+  const int RR = R * R;
+  double c5 = 0.0;
+  for (int c = lane; c < C; c += 32) {
+    const double* src = cd1 + (long long)c * H * H;
+    const double* ker = cw1 + c * RR;
+    for (int i = 0; i < R; ++i) {
+      const int hh = hb + i;
+      if (hh < 0 || hh >= H) continue;
+      for (int j = 0; j < R; ++j) {
+        const int ww = wb + j;
+        if (ww < 0 || ww >= H) continue;
+        c5 = fma(src[hh * H + ww], ker[i * R + j], c5);
+      }
+    }
+  }
+  const long long slab = (long long)N * E2;
+  const int terms = N * parts;
+  double s5 = 0.0;
+  for (int t = lane; t < terms; t += 32) {
+    const int q = t / N, n = t - q * N;
+    s5 += rowsum[q * slab + (long long)n * E2 + f];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c5 += __shfl_xor_sync(0xffffffffu, c5, o);
+    s5 += __shfl_xor_sync(0xffffffffu, s5, o);
+  }
+  if (lane == 0) {
+    if (bias) s5 -= (double)N * agg[0];
+    bool bad;
+    detect_one(c5, s5, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -435,6 +483,15 @@ int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N
                        const double* agg, double tau, DetectStats* st, cudaStream_t s) {
   FTC_LAUNCH(k_detect_warp<<<blocks_for((long long)E2 * 32), kThreads, 0, s>>>(co5, rowsum, parts, N, E2,
                                                                               bias, agg, tau, st));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_fused(const double* cd1, const double* cw1, const double* rowsum, int parts, int N,
+                        int C, int H, int R, int U, int pad, int E, int bias, const double* agg,
+                        double tau, DetectStats* st, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_fused<<<blocks_for((long long)E * E * 32), kThreads, 0, s>>>(
+      cd1, cw1, rowsum, parts, N, C, H, R, U, pad, E, bias, agg, tau, st));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

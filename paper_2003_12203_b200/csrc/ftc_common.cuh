@@ -154,6 +154,10 @@ int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N
 int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s);
 int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s);
+// clean path CoC-D with Co5 computed in the same kernel
+int launch_detect_fused(const double* cd1, const double* cw1, const double* rowsum, int parts, int N,
+                        int C, int H, int R, int U, int pad, int E, int bias, const double* agg,
+                        double tau, DetectStats* st, cudaStream_t s);
 int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
                         DetectStats* st, cudaStream_t s);
 int launch_count_differ(const double* c, const double* s_, long long n, double tau, int* count,

@@ -233,15 +233,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
         }
       }
       const float* base = a.D + (long long)n * a.C * HH + (long long)xb * H + yb;
+      // software pipeline: the gathers of chunk kc+1 are in flight while chunk kc is
+      // split, waited for and stored into TMEM
+      float vn[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int2 tp = tab_s[hf * 16 + e];
+        const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+        vn[e] = ok ? __ldg(base + tp.x) : 0.f;
+      }
       for (int kc = 0; kc < a.nkc; ++kc, ++g) {
         const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-        const int2* tk = tab_s + kc * kBK + hf * 16;
         float v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int2 tp = tk[e];
-          const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
-          v[e] = ok ? __ldg(base + tp.x) : 0.f;
+        for (int e = 0; e < 16; ++e) v[e] = vn[e];
+        if (kc + 1 < a.nkc) {
+          const int2* tk = tab_s + (kc + 1) * kBK + hf * 16;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int2 tp = tk[e];
+            const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+            vn[e] = ok ? __ldg(base + tp.x) : 0.f;
+          }
         }
         uint32_t hi[16], lo[16];
 #pragma unroll

@@ -113,6 +113,8 @@ struct ftc_layer {
   float* O = nullptr;
   int nfaults = 0, n_out_faults = 0;
   bool ck_exact = false;  // cd1/cd2 hold exact-order input checksums of D
+  const double* cd_ext1 = nullptr;  // producer-supplied exact checksums (read in place)
+  const double* cd_ext2 = nullptr;
   bool has_cd_faults = false;
   int rs_parts = 1;  // row-sum partial slabs written by the last fused-sum conv
   cudaStream_t stream = nullptr;
@@ -496,6 +498,11 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
 
   // The clean path may have produced only a fast Cd1: take the exact-order input
   // checksums of the caller's (pre-fault) D, re-applying injected checksum faults.
+  if (L->cd_ext1) {
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd1, L->cd_ext1, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, e.s));
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd2, L->cd_ext2, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, e.s));
+    L->cd_ext1 = L->cd_ext2 = nullptr;
+  }
   if (!L->ck_exact) {
     CK(launch_input_checksums(L->D, d.N, L->nCd, L->cd1, L->cd2, e.s));
     if (L->has_cd_faults) {
@@ -846,31 +853,43 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   // taken as given; otherwise a fast Cd1-only pass feeds CoC-D.
   L->has_cd_faults = L->nfaults && (has_target(faults, n_faults, FTC_FAULT_CD1) ||
                                     has_target(faults, n_faults, FTC_FAULT_CD2));
-  FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
-  FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
-  if (cd1_in) {
-    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd1, cd1_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
-    FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd2, cd2_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
+  const double* cd1_use = L->cd1;
+  L->cd_ext1 = L->cd_ext2 = nullptr;
+  bool side = false;
+  if (cd1_in && !L->has_cd_faults) {
+    // read the producer's checksums in place; copied into the layer only if the
+    // error path runs
+    cd1_use = cd1_in;
+    L->cd_ext1 = cd1_in;
+    L->cd_ext2 = cd2_in;
     L->ck_exact = true;
-  } else if (launch_cd1_fast(D, d.N, L->nCd, L->cd1, L->side) == FTC_OK) {
-    L->ck_exact = false;
   } else {
-    CK(launch_input_checksums(D, d.N, L->nCd, L->cd1, L->cd2, L->side));
-    L->ck_exact = true;
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
+    FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
+    side = true;
+    if (cd1_in) {
+      FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd1, cd1_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
+      FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd2, cd2_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
+      L->ck_exact = true;
+    } else if (launch_cd1_fast(D, d.N, L->nCd, L->cd1, L->side) == FTC_OK) {
+      L->ck_exact = false;
+    } else {
+      CK(launch_input_checksums(D, d.N, L->nCd, L->cd1, L->cd2, L->side));
+      L->ck_exact = true;
+    }
+    if (L->has_cd_faults) {
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, L->side));
+      if (L->ck_exact)
+        CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
+    }
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
   }
-  if (L->has_cd_faults) {
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, L->side));
-    if (L->ck_exact)
-      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
-  }
-  CK(launch_co5_fast(L->cd1, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, L->side));
-  FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
   // main stream: conv with fused post_conv faults and So2/So4 row sums
   CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
-  FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
+  if (side) FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
   FTC_CUDA_CHECK(cudaMemsetAsync(L->stats, 0, sizeof(DetectStats), s));
-  CK(launch_detect_warp(L->co5f, L->rowsum, L->rs_parts, d.N, L->E2, d.bias_enabled, L->agg, plan->tau,
-                        L->stats, s));
+  CK(launch_detect_fused(cd1_use, L->cw1, L->rowsum, L->rs_parts, d.N, d.C, d.H, d.R, d.stride, d.pad,
+                         L->E, d.bias_enabled, L->agg, plan->tau, L->stats, s));
   FTC_CUDA_CHECK(cudaMemcpyAsync(L->stats_h, L->stats, sizeof(DetectStats), cudaMemcpyDeviceToHost, s));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
   L->inflight = true;
@@ -932,6 +951,7 @@ int ftc_protected_check(ftc_layer* L, const ftc_plan* plan, const float* D, floa
   L->nfaults = 0;
   L->n_out_faults = 0;
   L->has_cd_faults = false;
+  L->cd_ext1 = L->cd_ext2 = nullptr;
   std::memset(rep, 0, sizeof *rep);
   // exact input checksums; detection is the error path's exact CoC-D
   CK(launch_input_checksums(D, L->d.N, L->nCd, L->cd1, L->cd2, s));
