@@ -29,8 +29,10 @@
 // partial of magnitude |O|*sqrt(32G/K), which bounds the loss at ~sqrt(96G) ulp(|O|)
 // independent of K; the partials are summed in registers (FP64 for BN <= 64, FP32
 // for wider tiles, where 64 doubles per thread would not fit).
-// Accumulators are double-buffered in TMEM so draining group g overlaps the MMAs
-// of group g+1.  TMEM: [0, 2*BN) accumulators, [2*BN, 2*BN+256) four A stages.
+// The two correction products go to a separate per-tile accumulator, so the main
+// one takes a third of the updates.  Main accumulators are double-buffered in TMEM
+// so draining group g overlaps the MMAs of group g+1.  TMEM: [0, 2*BN) main,
+// [2*BN, 3*BN) correction, then 2-4 A stages of 64 columns.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -42,7 +44,7 @@
 namespace ftc {
 
 struct TcPlan {
-  int BN = 0, ntiles = 0, nkc = 0, K = 0, M = 0, G = 2;
+  int BN = 0, ntiles = 0, nkc = 0, K = 0, M = 0, G = 1;
   float* Wp = nullptr;  // [ntiles][nkc][2][BN][32], SW128-swizzled, hi then lo
   int2* tab = nullptr;  // [nkc*32] im2col taps: {c*H*H + i*H + j, 1<<i | 1<<(16+j)}
 };
@@ -51,7 +53,13 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;
-constexpr int kStages = 4;
+// pipeline depth: TMEM holds 2*BN (main accumulators) + BN (correction accumulator)
+// + stages*64 (A hi/lo) columns of 512
+template <int BN>
+constexpr int stages_for() {
+  return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4);
+}
+constexpr int stages_rt(int BN) { return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4); }
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
 constexpr int kLoaderWarp = 8;
 constexpr int kMmaWarp = 9;
@@ -171,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* sptr = smem_raw + (sbase - raw);
+  constexpr int kStages = stages_for<BN>();
   const uint32_t stage_bytes = (uint32_t)BN * 256u;  // hi + lo tiles, 128 B per row each
   int2* tab_s = reinterpret_cast<int2*>(sptr + kStages * stage_bytes);
   const uint32_t tab_bytes = (uint32_t)a.nkc * kBK * 8u;
@@ -179,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   // bars: full[4], empty[4], acc_full[2], acc_empty[2], then tmem base (u32)
   const uint32_t full0 = bar_base, empty0 = bar_base + 8 * kStages;
   const uint32_t accf0 = bar_base + 16 * kStages, acce0 = accf0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t corrf = acce0 + 16, corre = corrf + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
@@ -192,6 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       mbar_init(accf0 + 8 * b, 1);
       mbar_init(acce0 + 8 * b, kEpiThreads);
     }
+    mbar_init(corrf, 1);
+    mbar_init(corre, kEpiThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kLoaderWarp) {
@@ -202,7 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t a_col0 = (uint32_t)(2 * BN);
+  const uint32_t corr_col = (uint32_t)(2 * BN);  // correction accumulator (per tile)
+  const uint32_t a_col0 = (uint32_t)(3 * BN);
 
   const int E = a.E, E2 = E * E, H = a.H, R = a.R, RR = R * R, HH = H * H;
   const int ntile_total = a.ntiles * a.npt;
@@ -297,8 +310,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       // kind::tf32, D=F32, A/B = TF32, K-major, M = 128, N = BN
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
-      uint32_t g = 0, gc = 0;
-      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+      uint32_t g = 0, gc = 0, tl = 0;
+      const uint32_t d_corr = tmem + corr_col;
+      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tl) {
+        // the correction accumulator collects lo*Bhi + hi*Blo over the whole tile
+        // (2^-11 of the magnitude: its truncation is negligible); the main one only
+        // the hi*Bhi products and is drained every G chunks
+        mbar_wait(corre, (tl & 1u) ^ 1u);
+        tc_after();
         for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
           const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
           mbar_wait(acce0 + 8 * acc, aph ^ 1u);
@@ -315,14 +334,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
             for (int k8 = 0; k8 < 4; ++k8) {
               const uint64_t dh = desc_sw128(b_hi + k8 * 32u);
               const uint64_t dl = desc_sw128(b_lo + k8 * 32u);
-              mma_tf32_ts(d_tmem, a_lo + k8 * 8u, dh, idesc, (kc != kc0 || k8 != 0) ? 1u : 0u);
-              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, dl, idesc, 1u);
-              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, dh, idesc, 1u);
+              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, dh, idesc, (kc != kc0 || k8 != 0) ? 1u : 0u);
+              mma_tf32_ts(d_corr, a_lo + k8 * 8u, dh, idesc, (kc != 0 || k8 != 0) ? 1u : 0u);
+              mma_tf32_ts(d_corr, a_hi + k8 * 8u, dl, idesc, 1u);
             }
             mma_commit(empty0 + 8 * s);
           }
           mma_commit(accf0 + 8 * acc);
         }
+        mma_commit(corrf);
       }
     }
   } else {
@@ -333,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     const int half = ew >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    uint32_t gc = 0;
-    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+    uint32_t gc = 0, tl = 0;
+    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tl) {
       const int nt = t / a.npt;
       const int pt = a.pt_lo + t % a.npt;
       const long long p = (long long)pt * kBM + r;
@@ -364,6 +384,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
         }
         tc_before();
         mbar_arrive(acce0 + 8 * acc);
+      }
+      {  // the tile's correction accumulator
+        mbar_wait(corrf, tl & 1u);
+        tc_after();
+        const uint32_t base = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
+#pragma unroll
+        for (int c16 = 0; c16 < HALF / 16; ++c16) {
+          uint32_t v[16];
+          tmem_ld16(base + (uint32_t)c16 * 16u, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
+        }
+        tc_before();
+        mbar_arrive(corre);
       }
       double rs = 0.0, rsm = 0.0;
       float* Obase = a.O + (long long)n * a.M * E2 + f;
@@ -456,7 +491,7 @@ bool tc_supported(const ftc_conv_desc& d) {
   const long long K = (long long)d.C * d.R * d.R;
   const long long nkc = (K + kBK - 1) / kBK;
   const long long bn = d.M <= 128 ? ((d.M + 31) / 32) * 32 : 128;
-  if (1024 + kStages * bn * 256 + nkc * kBK * 8 + 256 > 227 * 1024) return false;
+  if (1024 + stages_rt((int)bn) * bn * 256 + nkc * kBK * 8 + 256 > 227 * 1024) return false;
   if ((long long)d.C * d.H * d.H >= (1LL << 31)) return false;
   const long long E = (d.H + 2LL * d.pad - d.R) / d.stride + 1;
   if ((long long)d.N * E * E >= (1LL << 31)) return false;
@@ -468,7 +503,7 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
   p->M = d.M;
   p->K = d.C * d.R * d.R;
   p->nkc = (p->K + kBK - 1) / kBK;
-  if (const char* g = getenv("FTC_TC_DRAIN_CHUNKS")) p->G = atoi(g) > 0 ? atoi(g) : 2;
+  if (const char* g = getenv("FTC_TC_DRAIN_CHUNKS")) p->G = atoi(g) > 0 ? atoi(g) : 1;
   if (d.M <= 128) {
     p->BN = ((d.M + 31) / 32) * 32;
     p->ntiles = 1;
@@ -557,7 +592,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   }
   const int tiles = a.ntiles * a.npt;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  const size_t smem = 1024 + (size_t)kStages * p->BN * 256 + (size_t)p->nkc * kBK * 8 + 256;
+  const size_t smem = 1024 + (size_t)stages_rt(p->BN) * p->BN * 256 + (size_t)p->nkc * kBK * 8 + 256;
   switch (p->BN) {
     case 32: return launch_bn<32>(a, grid, smem, s);
     case 64: return launch_bn<64>(a, grid, smem, s);
