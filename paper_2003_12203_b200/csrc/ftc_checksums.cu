@@ -5,6 +5,7 @@
 // T=double the results are bitwise equal to checksums.hpp on the same FP32 data;
 // the clean-path detection (Co5 fast, fused So5) trades that for parallelism.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "ftc_common.cuh"
 
@@ -289,29 +290,35 @@ __global__ void k_count_differ(const double* __restrict__ c, const double* __res
 // families of the error path, which recomputes both exactly).  Two positions per
 // thread, eight images in flight per thread: enough bytes in flight to stream D at
 // HBM rate.
-__global__ void __launch_bounds__(128) k_cd1_fast(const float* __restrict__ D, int N, long long per2,
+__global__ void __launch_bounds__(128) k_cd1_fast(const float* __restrict__ D, int N, long long per4,
                                                   double* __restrict__ cd1) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= per2) return;
-  const float2* src = reinterpret_cast<const float2*>(D) + e;
-  double a0 = 0.0, a1 = 0.0;
+  if (e >= per4) return;
+  const float4* src = reinterpret_cast<const float4*>(D) + e;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int n = 0;
-  for (; n + 8 <= N; n += 8) {
-    float2 v[8];
+  for (; n + 16 <= N; n += 16) {
+    float4 v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (long long)(n + u) * per2);
+    for (int u = 0; u < 16; ++u) v[u] = __ldcs(src + (long long)(n + u) * per4);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       a0 += v[u].x;
       a1 += v[u].y;
+      a2 += v[u].z;
+      a3 += v[u].w;
     }
   }
   for (; n < N; ++n) {
-    const float2 v = __ldcs(src + (long long)n * per2);
+    const float4 v = __ldcs(src + (long long)n * per4);
     a0 += v.x;
     a1 += v.y;
+    a2 += v.z;
+    a3 += v.w;
   }
-  reinterpret_cast<double2*>(cd1)[e] = make_double2(a0, a1);
+  double2* o = reinterpret_cast<double2*>(cd1) + 2 * e;
+  o[0] = make_double2(a0, a1);
+  o[1] = make_double2(a2, a3);
 }
 
 // Clean-path CoC-D: one warp per position f; lanes stride over the (row-sum slab,
@@ -338,51 +345,133 @@ __global__ void k_detect_warp(const double* __restrict__ co5, const double* __re
   }
 }
 
-// Clean-path CoC-D in one kernel: per position f one warp computes
-//   Co5[f] = conv_block(Cd1, Cw1)[f]   (lanes over input channels, taps unrolled) and
-//   So5[f] = sum over the fused epilogue row sums (lanes over (slab, image) pairs),
-// both reduced with a fixed xor-shuffle tree, then compares them (values_differ).
-__global__ void k_detect_fused(const double* __restrict__ cd1, const double* __restrict__ cw1,
-                               const double* __restrict__ rowsum, int parts, int N, int C, int H,
-                               int R, int U, int pad, int E, int bias, const double* agg,
-                               double tau, DetectStats* st) {
+// Clean-path Co5 = conv_block(Cd1, Cw1) (checksums.hpp:157): a block owns 32
+// consecutive positions (lanes, coalesced Cd1 loads) x 16 channel slices (warps),
+// combined in a fixed order.  Runs on the side stream, concurrently with the conv.
+constexpr int kDetSlices = 16;
+template <int RT>  // RT > 0: compile-time kernel side (taps unrolled, loads issued first)
+__global__ void __launch_bounds__(32 * kDetSlices) k_co5_sliced(
+    const double* __restrict__ cd1, const double* __restrict__ cw1, double* __restrict__ co5, int C,
+    int H, int Rrt, int U, int pad, int E) {
+  __shared__ double red[kDetSlices][32];
+  const int R = RT > 0 ? RT : Rrt;
   const int E2 = E * E;
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (f >= E2) return;
-  const int x = f / E, y = f - (f / E) * E;
-  const int hb = x * U - pad, wb = y * U - pad;
-  const int RR = R * R;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane;
   double c5 = 0.0;
-  for (int c = lane; c < C; c += 32) {
-    const double* src = cd1 + (long long)c * H * H;
-    const double* ker = cw1 + c * RR;
-    for (int i = 0; i < R; ++i) {
-      const int hh = hb + i;
-      if (hh < 0 || hh >= H) continue;
-      for (int j = 0; j < R; ++j) {
-        const int ww = wb + j;
-        if (ww < 0 || ww >= H) continue;
-        c5 = fma(src[hh * H + ww], ker[i * R + j], c5);
+  if (f < E2) {
+    const int x = f / E, y = f - (f / E) * E;
+    const int hb = x * U - pad, wb = y * U - pad;
+    const int RR = R * R;
+    if constexpr (RT > 0) {
+      bool rok[RT], cok[RT];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        rok[i] = (unsigned)(hb + i) < (unsigned)H;
+        cok[i] = (unsigned)(wb + i) < (unsigned)H;
+      }
+      for (int c = w; c < C; c += kDetSlices) {
+        const double* src = cd1 + (long long)c * H * H + (long long)hb * H + wb;
+        const double* ker = cw1 + c * RR;
+        double v[RT * RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+          for (int j = 0; j < RT; ++j) v[i * RT + j] = (rok[i] && cok[j]) ? __ldg(src + i * H + j) : 0.0;
+#pragma unroll
+        for (int t = 0; t < RT * RT; ++t) c5 = fma(v[t], __ldg(ker + t), c5);
+      }
+    } else {
+      for (int c = w; c < C; c += kDetSlices) {
+        const double* src = cd1 + (long long)c * H * H;
+        const double* ker = cw1 + c * RR;
+        for (int i = 0; i < R; ++i) {
+          const int hh = hb + i;
+          if (hh < 0 || hh >= H) continue;
+          for (int j = 0; j < R; ++j) {
+            const int ww = wb + j;
+            if (ww < 0 || ww >= H) continue;
+            c5 = fma(src[hh * H + ww], ker[i * R + j], c5);
+          }
+        }
       }
     }
   }
-  const long long slab = (long long)N * E2;
-  const int terms = N * parts;
-  double s5 = 0.0;
-  for (int t = lane; t < terms; t += 32) {
-    const int q = t / N, n = t - q * N;
-    s5 += rowsum[q * slab + (long long)n * E2 + f];
-  }
+  red[w][lane] = c5;
+  __syncthreads();
+  if (w == 0 && f < E2) {
+    double cc = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c5 += __shfl_xor_sync(0xffffffffu, c5, o);
-    s5 += __shfl_xor_sync(0xffffffffu, s5, o);
+    for (int q = 0; q < kDetSlices; ++q) cc += red[q][lane];
+    co5[f] = cc;
   }
-  if (lane == 0) {
-    if (bias) s5 -= (double)N * agg[0];
-    bool bad;
-    detect_one(c5, s5, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
+}
+
+// Clean-path CoC-D after the conv: So5[f] = sum of the fused epilogue row sums over
+// (slab, image) (16 slices per 32 positions, fixed-order combine), compared with the
+// precomputed Co5 (values_differ).  The last block to finish publishes {flagged,
+// max_rel_dev} into the mapped host record and re-zeroes the device counters for
+// the next call (no memset / copy nodes on the clean path).
+__global__ void __launch_bounds__(32 * kDetSlices) k_detect_so5(
+    const double* __restrict__ co5, const double* __restrict__ rowsum, int parts, int N, int E2,
+    int bias, const double* agg, double tau, DetectStats* st, unsigned int* ticket,
+    DetectStats* host_out) {
+  __shared__ double red[kDetSlices][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane;
+  double s5 = 0.0;
+  if (f < E2) {
+    const long long slab = (long long)N * E2;
+    const int terms = N * parts;
+    for (int t = w; t < terms; t += kDetSlices) {
+      const int q = t / N, n = t - q * N;
+      s5 += rowsum[q * slab + (long long)n * E2 + f];
+    }
+  }
+  red[w][lane] = s5;
+  __syncthreads();
+  if (w == 0) {
+    int bad = 0;
+    unsigned long long devb = 0ull;
+    if (f < E2) {
+      double ss = 0.0;
+#pragma unroll
+      for (int q = 0; q < kDetSlices; ++q) ss += red[q][lane];
+      if (bias) ss -= (double)N * agg[0];
+      const double c = co5[f];
+      double den = fabs(c);
+      if (den < fabs(ss)) den = fabs(ss);
+      if (den < 1.0) den = 1.0;
+      const double dev = fabs(c - ss) / den;
+      if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
+      bad = values_differ(c, ss, tau) ? 1 : 0;
+    }
+    // one atomic per block (non-negative doubles order as u64; NaN devs excluded)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+      devb = other > devb ? other : devb;
+    }
+    if (lane == 0) {
+      if (bad) atomicAdd(&st->flagged, bad);
+      if (devb) atomicMax(&st->max_rel_dev_bits, devb);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(ticket, 1u);
+    if (done == gridDim.x - 1) {  // last block: publish and reset
+      __threadfence();
+      const int fl = atomicExch(&st->flagged, 0);
+      const unsigned long long mb = atomicExch(&st->max_rel_dev_bits, 0ull);
+      volatile DetectStats* h = host_out;
+      h->flagged = fl;
+      h->max_rel_dev_bits = mb;
+      __threadfence_system();
+      *ticket = 0u;
+    }
   }
 }
 
@@ -470,11 +559,11 @@ int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N
 }
 
 int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s) {
-  if (per % 2 != 0 || ((uintptr_t)D % 8) != 0) {
-    // odd plane size: the exact kernel also produces Cd1 (Cd2 into the same scratch)
+  if (per % 4 != 0 || ((uintptr_t)D % 16) != 0 || ((uintptr_t)cd1 % 16) != 0) {
+    // plane size not a multiple of 4: the exact kernel produces Cd1 (and Cd2)
     return FTC_CONFIG_ERROR;
   }
-  FTC_LAUNCH(k_cd1_fast<<<blocks_for(per / 2, 128), 128, 0, s>>>(D, N, per / 2, cd1));
+  FTC_LAUNCH(k_cd1_fast<<<blocks_for(per / 4, 128), 128, 0, s>>>(D, N, per / 4, cd1));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -487,11 +576,25 @@ int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N
   return FTC_OK;
 }
 
-int launch_detect_fused(const double* cd1, const double* cw1, const double* rowsum, int parts, int N,
-                        int C, int H, int R, int U, int pad, int E, int bias, const double* agg,
-                        double tau, DetectStats* st, cudaStream_t s) {
-  FTC_LAUNCH(k_detect_fused<<<blocks_for((long long)E * E * 32), kThreads, 0, s>>>(
-      cd1, cw1, rowsum, parts, N, C, H, R, U, pad, E, bias, agg, tau, st));
+int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
+                      int pad, int E, cudaStream_t s) {
+  const int g = (E * E + 31) / 32, t = 32 * kDetSlices;
+  switch (R) {
+    case 1: FTC_LAUNCH(k_co5_sliced<1><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+    case 3: FTC_LAUNCH(k_co5_sliced<3><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+    case 5: FTC_LAUNCH(k_co5_sliced<5><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+    case 7: FTC_LAUNCH(k_co5_sliced<7><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+    default: FTC_LAUNCH(k_co5_sliced<0><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+  }
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+                      const double* agg, double tau, DetectStats* st, unsigned int* ticket,
+                      DetectStats* host_out, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_so5<<<(E2 + 31) / 32, 32 * kDetSlices, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg,
+                                                                      tau, st, ticket, host_out));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

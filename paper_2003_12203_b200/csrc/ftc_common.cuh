@@ -155,9 +155,14 @@ int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStrea
 int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s);
 // clean path CoC-D with Co5 computed in the same kernel
-int launch_detect_fused(const double* cd1, const double* cw1, const double* rowsum, int parts, int N,
-                        int C, int H, int R, int U, int pad, int E, int bias, const double* agg,
-                        double tau, DetectStats* st, cudaStream_t s);
+// clean path: Co5 on the side stream, then So5 from the fused row sums + compare;
+// the last block publishes the record into mapped host memory (host_out) and
+// re-zeroes st/ticket for the next call
+int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
+                      int pad, int E, cudaStream_t s);
+int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+                      const double* agg, double tau, DetectStats* st, unsigned int* ticket,
+                      DetectStats* host_out, cudaStream_t s);
 int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,
                         DetectStats* st, cudaStream_t s);
 int launch_count_differ(const double* c, const double* s_, long long n, double tau, int* count,

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -65,6 +66,10 @@ struct ftc_layer {
   double *rowsum = nullptr, *rowsum_m = nullptr;
   DetectStats* stats = nullptr;
   DetectStats* stats_h = nullptr;  // pinned
+  DetectStats* fstats = nullptr;   // clean-path counters (kept zero between calls)
+  unsigned int* fticket = nullptr;
+  DetectStats* fstats_h = nullptr;  // mapped pinned record written by the detector
+  DetectStats* fstats_hd = nullptr; // its device alias
   ftc_fault* faults_dev = nullptr;
   ftc_fault* faults_h = nullptr;  // pinned staging
   int faults_cap = 0;
@@ -257,6 +262,9 @@ void free_layer(ftc_layer* L) {
   F(L->touched1); F(L->patches.n); F(L->patches.m); F(L->patches.f); F(L->patches.d); F(L->res);
   F(L->colmask); F(L->rowmask); F(L->colany); F(L->rowany); F(L->plane_mask); F(L->iscratch);
   if (L->stats_h) cudaFreeHost(L->stats_h);
+  if (L->fstats_h) cudaFreeHost(L->fstats_h);
+  F(L->fstats);
+  F(L->fticket);
   if (L->faults_h) cudaFreeHost(L->faults_h);
   if (L->res_h) cudaFreeHost(L->res_h);
   if (L->iscratch_h) cudaFreeHost(L->iscratch_h);
@@ -716,6 +724,12 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
     return fail(st);
   if (cudaMallocHost((void**)&L->stats_h, sizeof(DetectStats)) != cudaSuccess)
     return fail(FTC_CUDA_ERROR);
+  if ((st = dalloc(&L->fstats, 1)) || (st = dalloc(&L->fticket, 1))) return fail(st);
+  if (cudaMemset(L->fstats, 0, sizeof(DetectStats)) != cudaSuccess ||
+      cudaMemset(L->fticket, 0, sizeof(unsigned int)) != cudaSuccess ||
+      cudaHostAlloc((void**)&L->fstats_h, sizeof(DetectStats), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&L->fstats_hd, L->fstats_h, 0) != cudaSuccess)
+    return fail(FTC_CUDA_ERROR);
   if (cudaMemcpy(L->W, W_host, L->nW * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(FTC_CUDA_ERROR);
   if (desc->bias_enabled) {
@@ -855,7 +869,11 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
                                     has_target(faults, n_faults, FTC_FAULT_CD2));
   const double* cd1_use = L->cd1;
   L->cd_ext1 = L->cd_ext2 = nullptr;
-  bool side = false;
+  // The conv is enqueued first so its persistent CTAs are dispatched before the
+  // side-stream checksum work, which then fills the SM resources they leave free.
+  FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
+  CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
+  FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
   if (cd1_in && !L->has_cd_faults) {
     // read the producer's checksums in place; copied into the layer only if the
     // error path runs
@@ -864,9 +882,6 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     L->cd_ext2 = cd2_in;
     L->ck_exact = true;
   } else {
-    FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
-    FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
-    side = true;
     if (cd1_in) {
       FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd1, cd1_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
       FTC_CUDA_CHECK(cudaMemcpyAsync(L->cd2, cd2_in, L->nCd * sizeof(double), cudaMemcpyDeviceToDevice, L->side));
@@ -882,15 +897,12 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
       if (L->ck_exact)
         CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
     }
-    FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
   }
-  // main stream: conv with fused post_conv faults and So2/So4 row sums
-  CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
-  if (side) FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
-  FTC_CUDA_CHECK(cudaMemsetAsync(L->stats, 0, sizeof(DetectStats), s));
-  CK(launch_detect_fused(cd1_use, L->cw1, L->rowsum, L->rs_parts, d.N, d.C, d.H, d.R, d.stride, d.pad,
-                         L->E, d.bias_enabled, L->agg, plan->tau, L->stats, s));
-  FTC_CUDA_CHECK(cudaMemcpyAsync(L->stats_h, L->stats, sizeof(DetectStats), cudaMemcpyDeviceToHost, s));
+  CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, L->side));
+  FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
+  FTC_CUDA_CHECK(cudaStreamWaitEvent(s, L->ev_ck, 0));
+  CK(launch_detect_so5(L->co5f, L->rowsum, L->rs_parts, d.N, L->E2, d.bias_enabled, L->agg, plan->tau,
+                       L->fstats, L->fticket, L->fstats_hd, s));
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
   L->inflight = true;
   return FTC_OK;
@@ -918,12 +930,13 @@ int ftc_protected_conv_finish(ftc_layer* L, ftc_layer_report* rep) {
   const auto t1 = std::chrono::steady_clock::now();
   rep->t_detect_ms = std::chrono::duration<double, std::milli>(t1 - L->t0).count();
   {
-    unsigned long long b = L->stats_h->max_rel_dev_bits;
+    unsigned long long b = ((volatile DetectStats*)L->fstats_h)->max_rel_dev_bits;
     std::memcpy(&rep->max_rel_dev, &b, sizeof(double));
   }
-  rep->n_flagged = L->stats_h->flagged;
+  const int flagged = ((volatile DetectStats*)L->fstats_h)->flagged;
+  rep->n_flagged = flagged;
   int st = FTC_OK;
-  if (L->stats_h->flagged == 0) {
+  if (flagged == 0) {
     rep->detected = 0;
     rep->stage = FTC_STAGE_NONE;
   } else {
