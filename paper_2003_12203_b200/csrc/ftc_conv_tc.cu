@@ -45,8 +45,14 @@ namespace ftc {
 
 struct TcPlan {
   int BN = 0, ntiles = 0, nkc = 0, K = 0, M = 0, G = 1;
+  // channel-last gather (C % 32 == 0): the input is transposed to NHWC per launch and
+  // K runs tap-major (k = (i*R + j)*C + c), so a K chunk is 32 consecutive channels of
+  // one tap: one bounds test and four 16-byte loads per producer thread per chunk
+  bool nhwc = false;
   float* Wp = nullptr;  // [ntiles][nkc][2][BN][32], SW128-swizzled, hi then lo
-  int2* tab = nullptr;  // [nkc*32] im2col taps: {c*H*H + i*H + j, 1<<i | 1<<(16+j)}
+  int2* tab = nullptr;  // NCHW: [nkc*32] per-column taps {c*H*H + i*H + j, 1<<i | 1<<(16+j)}
+                        // NHWC: [nkc] per-chunk taps {(i*H + j)*C + c0, same bits}
+  float* Dt = nullptr;  // NHWC copy of the input (N*H*H*C), nhwc only
 };
 
 namespace {
@@ -59,7 +65,7 @@ template <int BN>
 constexpr int stages_for() {
   return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4);
 }
-constexpr int stages_rt(int BN) { return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4); }
+constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
 constexpr int kLoaderWarp = 8;
 constexpr int kMmaWarp = 9;
@@ -75,6 +81,8 @@ struct TcArgs {
   float* O;
   int N, C, H, M, R, U, pad, E, K, nkc, BN, ntiles;
   int G;           // K chunks per accumulator drain
+  int SB;          // B (shared-memory) pipeline stages
+  int dbg;         // FTC_TC_DEBUG bits (profiling experiments only; 0 in production)
   int pt_lo, npt;  // pixel tiles [pt_lo, pt_lo + npt)
   long long P;     // N*E*E
   const ftc_fault* faults;
@@ -119,6 +127,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}\n"
+      : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -134,6 +149,14 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -172,38 +195,73 @@ __device__ __forceinline__ float tf32_rn(float v) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <int BN>
+// Out of line: the store loop is unrolled over every column of the tile and an inlined
+// fault loop + mask lookup per column made the epilogue ~200 KB of SASS (instruction-
+// cache bound, ~40K cycles per tile).  Faults and repair masks are rare; a call is fine.
+// profiling aid (FTC_TC_DEBUG bit 64, block 0 only): per-chunk event clocks
+__device__ long long g_tc_trace[10][1024];
+#define TC_TRACE(on, slot, idx)                                  \
+  do {                                                           \
+    if ((on) && (idx) < 1024u) g_tc_trace[slot][idx] = clock64(); \
+  } while (0)
+
+struct HookOut {
+  float v;
+  int store;
+};
+__device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int y, const ftc_fault* f, int nf,
+                                               const uint32_t* plane_mask, int M) {
+  HookOut h;
+  h.v = nf ? apply_output_faults(v, n, m, x, y, f, nf) : v;
+  h.store = 1;
+  if (plane_mask) {
+    const long long pl = (long long)n * M + m;
+    h.store = (int)((plane_mask[pl >> 5] >> (pl & 31)) & 1u);
+  }
+  return h;
+}
+
+template <int BN, bool NHWC>
 __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the B stages (SW128 atoms)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   uint8_t* sptr = smem_raw + (sbase - raw);
-  constexpr int kStages = stages_for<BN>();
+  // A ring (TMEM, depth kSA) and B ring (shared memory, depth SB) advance together
+  // per K chunk but are sized independently: TMEM bounds A, shared memory bounds B.
+  constexpr int kMaxSB = 8;
+  const int SB = a.SB;
+  constexpr int kSA = stages_for<BN>();
   const uint32_t stage_bytes = (uint32_t)BN * 256u;  // hi + lo tiles, 128 B per row each
-  int2* tab_s = reinterpret_cast<int2*>(sptr + kStages * stage_bytes);
+  int2* tab_s = reinterpret_cast<int2*>(sptr + SB * stage_bytes);
   const uint32_t tab_bytes = (uint32_t)a.nkc * kBK * 8u;
-  const uint32_t bar_base = sbase + kStages * stage_bytes + tab_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + kStages * stage_bytes + tab_bytes);
-  // bars: full[4], empty[4], acc_full[2], acc_empty[2], then tmem base (u32)
-  const uint32_t full0 = bar_base, empty0 = bar_base + 8 * kStages;
-  const uint32_t accf0 = bar_base + 16 * kStages, acce0 = accf0 + 16;
+  const uint32_t bar_base = sbase + SB * stage_bytes + tab_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + SB * stage_bytes + tab_bytes);
+  // bars: fullA[4] emptyA[4] fullB[8] emptyB[8] accf[2] acce[2] corrf corre, tmem base
+  const uint32_t fullA0 = bar_base, emptyA0 = bar_base + 8 * 4;
+  const uint32_t fullB0 = bar_base + 8 * 8, emptyB0 = fullB0 + 8 * kMaxSB;
+  const uint32_t accf0 = emptyB0 + 8 * kMaxSB, acce0 = accf0 + 16;
   const uint32_t corrf = acce0 + 16, corre = corrf + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kMaxSB + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(full0 + 8 * s, kProdWarps * 32 + 1);
-      mbar_init(empty0 + 8 * s, 1);
+    for (int s = 0; s < kSA; ++s) {
+      mbar_init(fullA0 + 8 * s, kProdWarps);
+      mbar_init(emptyA0 + 8 * s, 1);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(fullB0 + 8 * s, 1);
+      mbar_init(emptyB0 + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, kEpiThreads);
+      mbar_init(acce0 + 8 * b, kEpiThreads / 32);
     }
     mbar_init(corrf, 1);
-    mbar_init(corre, kEpiThreads);
+    mbar_init(corre, kEpiThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kLoaderWarp) {
@@ -229,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     const int r = q * 32 + lane;  // row of the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t g = 0;
+    const bool pprof = (a.dbg & 64) && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kProdWarps - 1);
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
       const int pt = a.pt_lo + t % a.npt;
       const long long p = (long long)pt * kBM + r;
@@ -245,30 +304,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
           if ((unsigned)(yb + i) < (unsigned)H) okmask |= 1u << (16 + i);
         }
       }
-      const float* base = a.D + (long long)n * a.C * HH + (long long)xb * H + yb;
+      const float* base = NHWC ? a.D + (((long long)n * H + xb) * H + yb) * a.C + hf * 16
+                               : a.D + (long long)n * a.C * HH + (long long)xb * H + yb;
       // software pipeline: the gathers of chunk kc+1 are in flight while chunk kc is
       // split, waited for and stored into TMEM
-      float vn[16];
+      auto gather = [&](int kc, float (&out)[16]) {
+        if constexpr (NHWC) {
+          const int2 tp = tab_s[kc];
+          const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+          const float4* src = reinterpret_cast<const float4*>(base + tp.x);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int2 tp = tab_s[hf * 16 + e];
-        const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
-        vn[e] = ok ? __ldg(base + tp.x) : 0.f;
-      }
-      for (int kc = 0; kc < a.nkc; ++kc, ++g) {
-        const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-        float v[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = vn[e];
-        if (kc + 1 < a.nkc) {
-          const int2* tk = tab_s + (kc + 1) * kBK + hf * 16;
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 f = ok ? __ldg(src + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            out[4 * q4 + 0] = f.x;
+            out[4 * q4 + 1] = f.y;
+            out[4 * q4 + 2] = f.z;
+            out[4 * q4 + 3] = f.w;
+          }
+        } else {
+          const int2* tk = tab_s + kc * kBK + hf * 16;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int2 tp = tk[e];
             const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
-            vn[e] = ok ? __ldg(base + tp.x) : 0.f;
+            out[e] = ok ? __ldg(base + tp.x) : 0.f;
           }
         }
+      };
+      float vn[16];
+      gather(0, vn);
+      for (int kc = 0; kc < a.nkc; ++kc, ++g) {
+        const uint32_t s = g % kSA, ph = (g / kSA) & 1u;
+        float v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = vn[e];
+        if (kc + 1 < a.nkc && !(a.dbg & 1)) gather(kc + 1, vn);
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -279,70 +349,123 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
           const float l = v[e] - __uint_as_float(h);
           lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
         }
-        mbar_wait(empty0 + 8 * s, ph ^ 1u);
+        if (warp == 0) TC_TRACE(pprof, 0, g);
+        mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+        if (warp == 0) TC_TRACE(pprof, 1, g);
         tc_after();
-        const uint32_t col = tmem + lane_off + a_col0 + s * 64u + (uint32_t)hf * 16u;
-        tmem_st16(col, hi);
-        tmem_st16(col + 32u, lo);
-        tmem_wait_st();
+        if (!(a.dbg & 2)) {
+          const uint32_t col = tmem + lane_off + a_col0 + s * 64u + (uint32_t)hf * 16u;
+          tmem_st16(col, hi);
+          tmem_st16(col + 32u, lo);
+          tmem_wait_st();
+        }
         tc_before();
-        mbar_arrive(full0 + 8 * s);
+        __syncwarp();  // one elected arrival per warp: 256 same-address arrivals cost ~500 cycles
+        if (lane == 0) mbar_arrive(fullA0 + 8 * s);
+        TC_TRACE(pprof, warp == 0 ? 2 : 3, g);
       }
     }
   } else if (warp == kLoaderWarp) {
     // ================= B loader =================
     if (lane == 0) {
-      uint32_t g = 0;
+      uint32_t g = 0, sB = 0, phB = 0;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
         const int nt = t / a.npt;
         const float* src = a.Wp + (long long)nt * a.nkc * 2 * BN * kBK;
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
-          const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-          mbar_wait(empty0 + 8 * s, ph ^ 1u);
-          mbar_arrive_expect_tx(full0 + 8 * s, stage_bytes);
-          bulk_g2s(sbase + s * stage_bytes, src + (long long)kc * 2 * BN * kBK, stage_bytes, full0 + 8 * s);
+          const uint32_t s = sB, ph = phB;
+          if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
+          mbar_wait(emptyB0 + 8 * s, ph ^ 1u);
+          TC_TRACE((a.dbg & 64) && blockIdx.x == 0, 8, g);
+          if (a.dbg & 16) {
+            mbar_arrive(fullB0 + 8 * s);
+          } else {
+            mbar_arrive_expect_tx(fullB0 + 8 * s, stage_bytes);
+            bulk_g2s(sbase + s * stage_bytes, src + (long long)kc * 2 * BN * kBK, stage_bytes, fullB0 + 8 * s);
+          }
         }
       }
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
-    if (lane == 0) {
+    // the whole warp runs the schedule (its ring state stays warp-uniform, in uniform
+    // registers); one elected lane issues each tcgen05.mma / commit
+    {
       // kind::tf32, D=F32, A/B = TF32, K-major, M = 128, N = BN
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
-      uint32_t g = 0, gc = 0, tl = 0;
       const uint32_t d_corr = tmem + corr_col;
-      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tl) {
-        // the correction accumulator collects lo*Bhi + hi*Blo over the whole tile
-        // (2^-11 of the magnitude: its truncation is negligible); the main one only
-        // the hi*Bhi products and is drained every G chunks
-        mbar_wait(corre, (tl & 1u) ^ 1u);
-        tc_after();
-        for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
-          const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
-          mbar_wait(acce0 + 8 * acc, aph ^ 1u);
+      // Flat schedule over (tile, chunk).  A tile's correction MMAs wait for the previous
+      // tile's correction drain only after its main MMAs are queued, so the tile seam
+      // does not idle the tensor pipe.  Per accumulator the accumulation order is fixed:
+      // main = hi*Bhi over k8; corr = lo*Bhi, hi*Blo over k8.
+      const int my_tiles = (int)blockIdx.x < ntile_total ? (ntile_total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+      const uint32_t total = (uint32_t)my_tiles * (uint32_t)a.nkc;
+      const bool mprof = (a.dbg & 64) && blockIdx.x == 0;
+      if (total) {
+        // ring positions advance incrementally: this is one thread's serial code, and a
+        // runtime division per chunk costs more than the barrier handshakes
+        uint32_t g = 0, gc = 0, tl = 0, sA = 0, phA = 0, sB = 0, phB = 0;
+        int kc = 0, kg = 0;
+        mbar_wait(fullB0, 0);
+        mbar_wait(fullA0, 0);
+        mbar_wait(acce0, 1u);
+        for (;;) {
+          const bool tile_end = kc == a.nkc - 1;
+          const bool grp_start = kg == 0;
+          const bool grp_end = tile_end || kg == a.G - 1;
+          const uint32_t acc = gc & 1u;
           tc_after();
+          TC_TRACE(mprof, 4, g);
           const uint32_t d_tmem = tmem + acc * (uint32_t)BN;
-          const int kc1 = min(a.nkc, kc0 + a.G);
-          for (int kc = kc0; kc < kc1; ++kc, ++g) {
-            const uint32_t s = g % kStages, ph = (g / kStages) & 1u;
-            mbar_wait(full0 + 8 * s, ph);
-            tc_after();
-            const uint32_t a_hi = tmem + a_col0 + s * 64u, a_lo = a_hi + 32u;
-            const uint32_t b_hi = sbase + s * stage_bytes, b_lo = b_hi + (uint32_t)BN * 128u;
+          const uint32_t a_hi = tmem + a_col0 + sA * 64u, a_lo = a_hi + 32u;
+          const uint32_t b_hi = sbase + sB * stage_bytes, b_lo = b_hi + (uint32_t)BN * 128u;
+          if (!(a.dbg & 8) && elect_one()) {
 #pragma unroll
-            for (int k8 = 0; k8 < 4; ++k8) {
-              const uint64_t dh = desc_sw128(b_hi + k8 * 32u);
-              const uint64_t dl = desc_sw128(b_lo + k8 * 32u);
-              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, dh, idesc, (kc != kc0 || k8 != 0) ? 1u : 0u);
-              mma_tf32_ts(d_corr, a_lo + k8 * 8u, dh, idesc, (kc != 0 || k8 != 0) ? 1u : 0u);
-              mma_tf32_ts(d_corr, a_hi + k8 * 8u, dl, idesc, 1u);
-            }
-            mma_commit(empty0 + 8 * s);
+            for (int k8 = 0; k8 < 4; ++k8)
+              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, desc_sw128(b_hi + k8 * 32u), idesc, (!grp_start || k8) ? 1u : 0u);
           }
-          mma_commit(accf0 + 8 * acc);
+          __syncwarp();
+          if (kc == 0) {
+            mbar_wait(corre, (tl & 1u) ^ 1u);
+            tc_after();
+          }
+          if (elect_one()) {
+            if (!(a.dbg & 8)) {
+#pragma unroll
+              for (int k8 = 0; k8 < 4; ++k8) {
+                mma_tf32_ts(d_corr, a_lo + k8 * 8u, desc_sw128(b_hi + k8 * 32u), idesc, (kc || k8) ? 1u : 0u);
+                mma_tf32_ts(d_corr, a_hi + k8 * 8u, desc_sw128(b_lo + k8 * 32u), idesc, 1u);
+              }
+            }
+            TC_TRACE(mprof, 5, g);
+            // release the stage first (the producers are on the critical path), then wait
+            // for the next chunk's operands / accumulator buffer
+            mma_commit(emptyA0 + 8 * sA);
+            mma_commit(emptyB0 + 8 * sB);
+            if (grp_end) mma_commit(accf0 + 8 * acc);
+            if (tile_end) mma_commit(corrf);
+          }
+          __syncwarp();
+          if (++g == total) break;
+          if (++sA == (uint32_t)kSA) { sA = 0; phA ^= 1u; }
+          if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
+          mbar_wait(fullB0 + 8 * sB, phB);
+          mbar_wait(fullA0 + 8 * sA, phA);
+          if (grp_end) {
+            ++gc;
+            kg = 0;
+            mbar_wait(acce0 + 8 * (gc & 1u), ((gc >> 1) & 1u) ^ 1u);
+          } else {
+            ++kg;
+          }
+          if (tile_end) {
+            ++tl;
+            kc = 0;
+          } else {
+            ++kc;
+          }
         }
-        mma_commit(corrf);
       }
     }
   } else {
@@ -354,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t gc = 0, tl = 0;
+    const bool eprof = (a.dbg & 64) && blockIdx.x == 0 && threadIdx.x == kEpiWarp0 * 32;
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tl) {
       const int nt = t / a.npt;
       const int pt = a.pt_lo + t % a.npt;
@@ -372,10 +496,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
         const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
         mbar_wait(accf0 + 8 * acc, aph);
+        TC_TRACE(eprof, 6, gc);
         tc_after();
         const uint32_t base = tmem + lane_off + acc * (uint32_t)BN + (uint32_t)(half * HALF);
 #pragma unroll
         for (int c16 = 0; c16 < HALF / 16; ++c16) {
+          if (a.dbg & 4) break;
           uint32_t v[16];
           tmem_ld16(base + (uint32_t)c16 * 16u, v);
           tmem_wait_ld();
@@ -383,52 +509,116 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
           for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
         }
         tc_before();
-        mbar_arrive(acce0 + 8 * acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acce0 + 8 * acc);
+        TC_TRACE(eprof, 7, gc);
       }
-      {  // the tile's correction accumulator
-        mbar_wait(corrf, tl & 1u);
-        tc_after();
-        const uint32_t base = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
+      // the tile's correction accumulator
+      mbar_wait(corrf, tl & 1u);
+      tc_after();
+      const uint32_t cbase = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
+#pragma unroll
+      for (int c16 = 0; c16 < HALF / 16; ++c16) {
+        uint32_t v[16];
+        tmem_ld16(cbase + (uint32_t)c16 * 16u, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
+      }
+      // tile store + fused FP64 row sums (m order, exact roundings).  Common case: a lean
+      // unrolled body after releasing the correction accumulator, so the stores overlap
+      // the next tile's MMAs.  Hooks (faults / repair mask) and partial column ranges:
+      // the values go back into TMEM and a rolled loop with one out-of-line call per
+      // column stores them (an unrolled hook body per column is instruction-cache bound).
+      double rs = 0.0, rsm = 0.0;
+      const int m0 = nt * BN + half * HALF;
+      const int mlim = min(HALF, a.M - m0);
+      float* op = a.O + ((long long)n * a.M + m0) * E2 + f;
+      const float* bp = a.bias ? a.bias + m0 : nullptr;
+      if (mlim == HALF && !a.nfaults && !a.plane_mask) {
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(corre);
+        if (valid) {
+          if (bp) {
+#pragma unroll
+            for (int jj = 0; jj < HALF; ++jj) {
+              const float val = (float)sum[jj] + __ldg(bp + jj);
+              op[jj * E2] = val;
+              rs = dadd(rs, (double)val);
+              rsm = dadd(rsm, dmul((double)(m0 + jj), (double)val));
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < HALF; ++jj) {
+              const float val = (float)sum[jj];
+              op[jj * E2] = val;
+              rs = dadd(rs, (double)val);
+              rsm = dadd(rsm, dmul((double)(m0 + jj), (double)val));
+            }
+          }
+        }
+      } else {
 #pragma unroll
         for (int c16 = 0; c16 < HALF / 16; ++c16) {
           uint32_t v[16];
-          tmem_ld16(base + (uint32_t)c16 * 16u, v);
-          tmem_wait_ld();
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
+          for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint((float)sum[c16 * 16 + jj]);
+          tmem_st16(cbase + (uint32_t)c16 * 16u, v);
+        }
+        tmem_wait_st();
+        const bool hooks = a.nfaults || a.plane_mask;
+#pragma unroll 1
+        for (int c0 = 0; c0 < mlim; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(cbase + (uint32_t)c0, v);
+          tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = c0 + jj;
+              if (j < mlim) {
+                float val = __uint_as_float(v[jj]);
+                if (bp) val = val + __ldg(bp + j);
+                int st = 1;
+                if (hooks) {
+                  const HookOut h = epilogue_hooks(val, n, m0 + j, x, y, a.faults, a.nfaults, a.plane_mask, a.M);
+                  val = h.v;
+                  st = h.store;
+                }
+                if (st) op[(long long)j * E2] = val;
+                rs = dadd(rs, (double)val);
+                rsm = dadd(rsm, dmul((double)(m0 + j), (double)val));
+              }
+            }
+          }
         }
         tc_before();
-        mbar_arrive(corre);
-      }
-      double rs = 0.0, rsm = 0.0;
-      float* Obase = a.O + (long long)n * a.M * E2 + f;
-#pragma unroll
-      for (int jj = 0; jj < HALF; ++jj) {
-        const int m = nt * BN + half * HALF + jj;
-        if (!valid || m >= a.M) continue;
-        float val = (float)sum[jj];
-        if (a.bias) val = val + __ldg(a.bias + m);
-        if (a.nfaults) val = apply_output_faults(val, n, m, x, y, a.faults, a.nfaults);
-        bool store = true;
-        if (a.plane_mask) {
-          const long long pl = (long long)n * a.M + m;
-          store = (a.plane_mask[pl >> 5] >> (pl & 31)) & 1u;
-        }
-        if (store) Obase[(long long)m * E2] = val;
-        const double dv = (double)val;
-        rs = dadd(rs, dv);
-        rsm = dadd(rsm, dmul((double)m, dv));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(corre);
       }
       if (valid && a.rowsum) {
         const long long o = (long long)(2 * nt + half) * a.P + p;
         a.rowsum[o] = rs;
         a.rowsum_m[o] = rsm;
       }
+      TC_TRACE(eprof, 9, tl);
     }
   }
   tc_before();
   __syncthreads();
   tc_after();
+  if ((a.dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_tc_trace[4][0];
+    printf("TRACE chunk: g Pws Pwe Parr P7arr Mready Missued Lb\n");
+    for (int g = 0; g < 400; ++g)
+      printf("TRACE c %d %lld %lld %lld %lld %lld %lld %lld\n", g, g_tc_trace[0][g] - t0, g_tc_trace[1][g] - t0,
+             g_tc_trace[2][g] - t0, g_tc_trace[3][g] - t0, g_tc_trace[4][g] - t0, g_tc_trace[5][g] - t0,
+             g_tc_trace[8][g] - t0);
+    for (int g = 0; g < 100; ++g)
+      printf("TRACE grp %d %lld %lld\n", g, g_tc_trace[6][g] - t0, g_tc_trace[7][g] - t0);
+    for (int g = 0; g < 6; ++g) printf("TRACE tile %d %lld\n", g, g_tc_trace[9][g] - t0);
+  }
   if (warp == kLoaderWarp) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -437,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
 // W -> [ntiles][nkc][hi,lo][BN][32] with the SW128 chunk swizzle (16-byte chunk
 // index XOR row%8), rows >= M and k >= K zero-padded.
 __global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, int M, int K, int BN,
-                         int ntiles, int nkc) {
+                         int ntiles, int nkc, int C, int RR, int tap_major) {
   const long long total = (long long)ntiles * nkc * BN * kBK;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -446,7 +636,9 @@ __global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, in
     const int kc = (int)((e / ((long long)kBK * BN)) % nkc);
     const int nt = (int)(e / ((long long)kBK * BN * nkc));
     const int m = nt * BN + row, kk = kc * kBK + k;
-    const float w = (m < M && kk < K) ? W[(long long)m * K + kk] : 0.f;
+    // tap-major K (NHWC gather): kk = t*C + c  <->  reference index c*RR + t
+    const long long src = tap_major ? (long long)m * K + (long long)(kk % C) * RR + kk / C : (long long)m * K + kk;
+    const float w = (m < M && kk < K) ? W[src] : 0.f;
     const float hi = tf32_rn(w), lo = tf32_rn(w - hi);
     const long long tile = ((long long)nt * nkc + kc) * 2;
     const int sw = row * kBK + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3);
@@ -468,17 +660,44 @@ __global__ void k_build_tab(int2* tab, int C, int H, int R, int K, int Kpad) {
   tab[k] = make_int2((c * H + i) * H + j, (int)((1u << i) | (1u << (16 + j))));
 }
 
+// per-chunk taps for the channel-last gather (C % 32 == 0, so a chunk never straddles taps)
+__global__ void k_build_tab_nhwc(int2* tab, int C, int H, int R, int nkc) {
+  const int kc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (kc >= nkc) return;
+  const int k0 = kc * kBK, t = k0 / C, c0 = k0 % C, i = t / R, j = t % R;
+  tab[kc] = make_int2((i * H + j) * C + c0, (int)((1u << i) | (1u << (16 + j))));
+}
+
+// D[n][c][hw] -> Dt[n][hw][c] for images [n_lo, n_lo + gridDim.z), 32x32 tiles
+__global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ D, float* __restrict__ Dt, int C,
+                                                     int HW, int n_lo) {
+  __shared__ float t[32][33];
+  const long long n = n_lo + blockIdx.z;
+  const int hw0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const float* src = D + n * C * HW;
+  float* dst = Dt + n * C * HW;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int c = c0 + r, hw = hw0 + threadIdx.x;
+    if (c < C && hw < HW) t[r][threadIdx.x] = __ldg(src + (long long)c * HW + hw);
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int hw = hw0 + r, c = c0 + threadIdx.x;
+    if (c < C && hw < HW) dst[(long long)hw * C + c] = t[threadIdx.x][r];
+  }
+}
+
 int g_num_sms = 0;
 
-template <int BN>
+template <int BN, bool NHWC>
 int launch_bn(const TcArgs& a, int grid, size_t smem, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, NHWC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     attr_set = true;
   }
-  FTC_LAUNCH(k_conv_tc<BN><<<grid, kThreads, smem, s>>>(a));
+  FTC_LAUNCH(k_conv_tc<BN, NHWC><<<grid, kThreads, smem, s>>>(a));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -491,7 +710,7 @@ bool tc_supported(const ftc_conv_desc& d) {
   const long long K = (long long)d.C * d.R * d.R;
   const long long nkc = (K + kBK - 1) / kBK;
   const long long bn = d.M <= 128 ? ((d.M + 31) / 32) * 32 : 128;
-  if (1024 + stages_rt((int)bn) * bn * 256 + nkc * kBK * 8 + 256 > 227 * 1024) return false;
+  if (1024 + stages_host(bn) * bn * 256 + nkc * kBK * 8 + 512 > 227 * 1024) return false;
   if ((long long)d.C * d.H * d.H >= (1LL << 31)) return false;
   const long long E = (d.H + 2LL * d.pad - d.R) / d.stride + 1;
   if ((long long)d.N * E * E >= (1LL << 31)) return false;
@@ -503,6 +722,10 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
   p->M = d.M;
   p->K = d.C * d.R * d.R;
   p->nkc = (p->K + kBK - 1) / kBK;
+  // main accumulator drained every 2 K chunks (64 K): the tensor core truncates its
+  // accumulator adds, so longer runs lose accuracy (G=3 already exceeds the reference's
+  // own FP32 error on ResNet-18's 1x1 projections); G=1 costs ~9% more on AlexNet conv2
+  p->G = 2;
   if (const char* g = getenv("FTC_TC_DRAIN_CHUNKS")) p->G = atoi(g) > 0 ? atoi(g) : 1;
   if (d.M <= 128) {
     p->BN = ((d.M + 31) / 32) * 32;
@@ -511,6 +734,9 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
     p->BN = 128;
     p->ntiles = (d.M + 127) / 128;
   }
+  // channel-last gather: faster producers, but with the MMA issue chain the bottleneck it
+  // does not pay for its transpose pass yet (AlexNet conv2 669 vs 641 us): opt-in
+  p->nhwc = d.C % 32 == 0 && getenv("FTC_TC_NHWC") != nullptr;
   if (const char* bn = getenv("FTC_TC_MAX_BN")) {  // experimentation: cap the N tile
     const int cap = atoi(bn);
     if ((cap == 32 || cap == 64 || cap == 96 || cap == 128) && p->BN > cap) {
@@ -524,15 +750,28 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
     set_error(FTC_CUDA_ERROR, "cudaMalloc(packed W) failed");
     return FTC_CUDA_ERROR;
   }
-  FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, d.M, p->K, p->BN, p->ntiles, p->nkc));
+  FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, d.M, p->K, p->BN, p->ntiles, p->nkc, d.C, d.R * d.R,
+                                         p->nhwc ? 1 : 0));
   if (cudaMalloc(&p->tab, (size_t)p->nkc * kBK * sizeof(int2)) != cudaSuccess) {
     cudaFree(p->Wp);
     delete p;
     set_error(FTC_CUDA_ERROR, "cudaMalloc(tap table) failed");
     return FTC_CUDA_ERROR;
   }
-  FTC_LAUNCH(k_build_tab<<<(p->nkc * kBK + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->K,
-                                                                   p->nkc * kBK));
+  if (p->nhwc) {
+    cudaMemsetAsync(p->tab, 0, (size_t)p->nkc * kBK * sizeof(int2), s);
+    FTC_LAUNCH(k_build_tab_nhwc<<<(p->nkc + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->nkc));
+    if (cudaMalloc(&p->Dt, (size_t)d.N * d.C * d.H * d.H * sizeof(float)) != cudaSuccess) {
+      cudaFree(p->Wp);
+      cudaFree(p->tab);
+      delete p;
+      set_error(FTC_CUDA_ERROR, "cudaMalloc(NHWC input copy) failed");
+      return FTC_CUDA_ERROR;
+    }
+  } else {
+    FTC_LAUNCH(k_build_tab<<<(p->nkc * kBK + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->K,
+                                                                     p->nkc * kBK));
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFree(p->Wp);
@@ -548,6 +787,7 @@ void tc_plan_destroy(TcPlan* p) {
   if (!p) return;
   if (p->Wp) cudaFree(p->Wp);
   if (p->tab) cudaFree(p->tab);
+  if (p->Dt) cudaFree(p->Dt);
   delete p;
 }
 
@@ -592,12 +832,39 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   }
   const int tiles = a.ntiles * a.npt;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  const size_t smem = 1024 + (size_t)stages_rt(p->BN) * p->BN * 256 + (size_t)p->nkc * kBK * 8 + 256;
-  switch (p->BN) {
-    case 32: return launch_bn<32>(a, grid, smem, s);
-    case 64: return launch_bn<64>(a, grid, smem, s);
-    case 96: return launch_bn<96>(a, grid, smem, s);
-    case 128: return launch_bn<128>(a, grid, smem, s);
+  // as many B stages as shared memory allows (2..8) after the tap table
+  const size_t fixed = 1024 + (size_t)p->nkc * kBK * 8 + 512;
+  int SB = (int)((227 * 1024 - fixed) / ((size_t)p->BN * 256));
+  SB = SB > 8 ? 8 : SB;
+  if (SB < stages_host(p->BN)) {
+    set_error(FTC_CONFIG_ERROR, "tcgen05 conv: shared memory too small for the B ring");
+    return FTC_CONFIG_ERROR;
+  }
+  if (const char* e = getenv("FTC_TC_B_STAGES")) {  // experimentation
+    const int v = atoi(e);
+    if (v >= stages_host(p->BN) && v < SB) SB = v;
+  }
+  a.SB = SB;
+  a.dbg = getenv("FTC_TC_DEBUG") ? atoi(getenv("FTC_TC_DEBUG")) : 0;
+  const size_t smem = fixed + (size_t)SB * p->BN * 256;
+  if (p->nhwc) {
+    const int nimg = c.img_hi - c.img_lo;
+    const dim3 tg((unsigned)((c.H * c.H + 31) / 32), (unsigned)(c.C / 32), (unsigned)nimg);
+    FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(c.D, p->Dt, c.C, c.H * c.H, c.img_lo));
+    a.D = p->Dt;
+    switch (p->BN) {
+      case 32: return launch_bn<32, true>(a, grid, smem, s);
+      case 64: return launch_bn<64, true>(a, grid, smem, s);
+      case 96: return launch_bn<96, true>(a, grid, smem, s);
+      case 128: return launch_bn<128, true>(a, grid, smem, s);
+    }
+  } else {
+    switch (p->BN) {
+      case 32: return launch_bn<32, false>(a, grid, smem, s);
+      case 64: return launch_bn<64, false>(a, grid, smem, s);
+      case 96: return launch_bn<96, false>(a, grid, smem, s);
+      case 128: return launch_bn<128, false>(a, grid, smem, s);
+    }
   }
   set_error(FTC_CONFIG_ERROR, "unsupported BN");
   return FTC_CONFIG_ERROR;
