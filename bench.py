@@ -283,7 +283,9 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        torch.cuda.nvtx.range_push("timed_step")  # ncu --nvtx --nvtx-include timed_step/
         wl.launch()
+        torch.cuda.nvtx.range_pop()
         e1.record(stream)
         reps = wl.finish()
         reports.append(reps)
@@ -336,8 +338,15 @@ def main():
         else:
             peak = 148 * 128 * 2 * 1.965e9 / 1e12
             basis = "FP32 SIMT FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz (derived)"
+        # DRAM traffic of the conv launches of one step, from the committed ncu --set full
+        # capture of the same workload (profiles/r01_traffic.json; AlexNet only)
+        traffic = None
+        tj = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if args.workload == "alexnet" and os.path.exists(tj):
+            traffic = json.load(open(tj))["conv_dram_bytes_per_step"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "conv (sum over layers per step)",
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (5 conv launches)",
+                "kernel": "conv (sum over layers per step)",
                 "kernel_ms_per_step": conv_avg_ms, "peak_basis": basis,
                 "flops_per_step": wl.flops}
         cpu = None

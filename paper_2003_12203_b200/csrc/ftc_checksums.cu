@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kThreads) k_input_checksums_v4(const float* __
   for (; n + 4 <= N; n += 4) {
     float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + (long long)(n + u) * per4);
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (long long)(n + u) * per4);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const double w = (double)(n + u);
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_input_checksums_v4(const float* __
     }
   }
   for (; n < N; ++n) {
-    const float4 v = __ldcs(src + (long long)n * per4);
+    const float4 v = __ldg(src + (long long)n * per4);
     const double w = (double)n;
     const double a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -71,8 +71,19 @@ __global__ void k_input_checksums_scalar(const float* __restrict__ D, int N, lon
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= per) return;
   double s1 = 0.0, s2 = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double v = D[(long long)n * per + e];
+  int n = 0;
+  for (; n + 16 <= N; n += 16) {  // 16 loads in flight, then the ordered adds
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldg(D + (long long)(n + u) * per + e);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      s1 = dadd(s1, (double)v[u]);
+      s2 = dadd(s2, dmul((double)(n + u), (double)v[u]));
+    }
+  }
+  for (; n < N; ++n) {
+    const double v = __ldg(D + (long long)n * per + e);
     s1 = dadd(s1, v);
     s2 = dadd(s2, dmul((double)n, v));
   }
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(128) k_cd1_fast(const float* __restrict__ D, i
     }
   }
   for (; n < N; ++n) {
-    const float4 v = __ldcs(src + (long long)n * per4);
+    const float4 v = __ldg(src + (long long)n * per4);
     a0 += v.x;
     a1 += v.y;
     a2 += v.z;
@@ -480,8 +491,10 @@ __global__ void __launch_bounds__(32 * kDetSlices) k_detect_so5(
 // ------------------------------------------------------------------ launchers
 int launch_input_checksums(const float* D, int N, long long per, double* cd1, double* cd2,
                            cudaStream_t s) {
-  const bool vec = (per % 4 == 0) && ((uintptr_t)D % 16 == 0) && ((uintptr_t)cd1 % 16 == 0) &&
-                   ((uintptr_t)cd2 % 16 == 0);
+  // vector form when there are enough positions to fill the GPU; otherwise one position
+  // per thread with 16 batch loads in flight (small planes are latency-bound)
+  const bool vec = (per % 4 == 0) && per >= 4 * 148 * 256 && ((uintptr_t)D % 16 == 0) &&
+                   ((uintptr_t)cd1 % 16 == 0) && ((uintptr_t)cd2 % 16 == 0);
   if (vec)
     FTC_LAUNCH(k_input_checksums_v4<<<blocks_for(per / 4), kThreads, 0, s>>>(D, N, per / 4, cd1, cd2));
   else

@@ -9,18 +9,19 @@
 // lo = RN_tf32(v - hi); each K step issues lo*Bhi + hi*Blo + hi*Bhi into one FP32
 // TMEM accumulator (the dropped lo*lo term is 2^-22 relative).
 //
-// Warp roles (persistent CTA per SM, 448 threads):
-//   warps 0-3  A producers: gather the im2col row of their pixel straight from D
-//              (L1/L2-resident halo), split hi/lo and tcgen05.st it into a TMEM
-//              stage (A operand of the TS-form MMA; no shared-memory round trip);
-//   warp 4     B loader: one cp.async.bulk per stage of the pre-packed, pre-split,
-//              pre-swizzled kernel tile (K-major SW128) into shared memory;
-//              also owns the TMEM allocation;
-//   warp 5     MMA issuer (one thread): 12 tcgen05.mma.kind::tf32 per K chunk;
-//   warps 6-13 epilogue (two warps per TMEM lane quarter, each owning half of the
-//              BN columns): drain the accumulator every G K-chunks into FP32
-//              register sums, then + bias, post_conv faults, coalesced NCHW
-//              store, fused FP64 row sums (So2/So4 partials).
+// Warp roles (persistent CTA per SM, 608 threads):
+//   warps 0-7   A producers (two per TMEM lane quarter): gather the im2col row of their
+//               pixel straight from D (L1/L2-resident halo), split hi/lo and tcgen05.st
+//               it into a TMEM half-stage (warps 0-3: K columns 0-15 of a chunk, 4-7:
+//               16-31) -- the A operand of the TS-form MMA, no shared-memory round trip;
+//   warp 8      B loader: one cp.async.bulk per stage of the pre-packed, pre-split,
+//               pre-swizzled kernel tile (K-major SW128); owns the TMEM allocation;
+//   warps 9-10  MMA issuers, one per half chunk (6 tcgen05.mma.kind::tf32 each),
+//               alternating under a turn barrier;
+//   warps 11-18 epilogue (two per TMEM lane quarter, each owning half of the BN
+//               columns): drain the accumulator every G K-chunks into register sums,
+//               then + bias, post_conv faults, coalesced NCHW store, fused FP64 row sums
+//               (So2/So4 partials).
 //
 // Why the drain: the tensor core aligns every addend to the accumulator's exponent
 // and drops the bits below its ulp, so one accumulator over the whole K loses
@@ -32,7 +33,7 @@
 // The two correction products go to a separate per-tile accumulator, so the main
 // one takes a third of the updates.  Main accumulators are double-buffered in TMEM
 // so draining group g overlaps the MMAs of group g+1.  TMEM: [0, 2*BN) main,
-// [2*BN, 3*BN) correction, then 2-4 A stages of 64 columns.
+// [2*BN, 3*BN) correction, then 4-8 A half-stages of 32 columns (16 hi + 16 lo).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -68,10 +69,10 @@ constexpr int stages_for() {
 constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
 constexpr int kLoaderWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kEpiWarp0 = 10;
+constexpr int kMmaWarp = 9;  // and 10: two issuers alternating K chunks
+constexpr int kEpiWarp0 = 11;
 constexpr int kEpiThreads = 256;
-constexpr int kThreads = 576;
+constexpr int kThreads = 608;
 
 struct TcArgs {
   const float* D;
@@ -238,18 +239,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const uint32_t tab_bytes = (uint32_t)a.nkc * kBK * 8u;
   const uint32_t bar_base = sbase + SB * stage_bytes + tab_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + SB * stage_bytes + tab_bytes);
-  // bars: fullA[4] emptyA[4] fullB[8] emptyB[8] accf[2] acce[2] corrf corre, tmem base
-  const uint32_t fullA0 = bar_base, emptyA0 = bar_base + 8 * 4;
-  const uint32_t fullB0 = bar_base + 8 * 8, emptyB0 = fullB0 + 8 * kMaxSB;
+  // A ring of half-stages: a K chunk's first 16 columns (hf = 0) and last 16 (hf = 1)
+  // are separate stages of 32 TMEM columns (16 hi + 16 lo), filled by their own producer
+  // warps and released after their own 6 MMAs -- the refill of a stage overlaps 3 half
+  // chunks of MMAs instead of 1 whole chunk
+  constexpr int kHS = 2 * kSA;
+  // bars: fullA[8] emptyA[8] fullB[8] emptyB[8] accf[2] acce[2] corrf corre turn, tmem base
+  const uint32_t fullA0 = bar_base, emptyA0 = bar_base + 8 * 8;
+  const uint32_t fullB0 = bar_base + 8 * 16, emptyB0 = fullB0 + 8 * kMaxSB;
   const uint32_t accf0 = emptyB0 + 8 * kMaxSB, acce0 = accf0 + 16;
-  const uint32_t corrf = acce0 + 16, corre = corrf + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kMaxSB + 6);
+  const uint32_t corrf = acce0 + 16, corre = corrf + 8, turn = corre + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kMaxSB + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSA; ++s) {
-      mbar_init(fullA0 + 8 * s, kProdWarps);
+    for (int s = 0; s < kHS; ++s) {
+      mbar_init(fullA0 + 8 * s, kProdWarps / 2);
       mbar_init(emptyA0 + 8 * s, 1);
     }
     for (int s = 0; s < SB; ++s) {
@@ -262,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     }
     mbar_init(corrf, 1);
     mbar_init(corre, kEpiThreads / 32);
+    mbar_init(turn, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kLoaderWarp) {
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     const int q = warp & 3, hf = warp >> 2;
     const int r = q * 32 + lane;  // row of the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    uint32_t g = 0;
+    uint32_t g = 0, hs = (uint32_t)hf, hph = 0;  // this warp's half-stage slot / phase
     const bool pprof = (a.dbg & 64) && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kProdWarps - 1);
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
       const int pt = a.pt_lo + t % a.npt;
@@ -334,7 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
       float vn[16];
       gather(0, vn);
       for (int kc = 0; kc < a.nkc; ++kc, ++g) {
-        const uint32_t s = g % kSA, ph = (g / kSA) & 1u;
+        const uint32_t s = hs, ph = hph;
+        hs += 2;
+        if (hs >= (uint32_t)kHS) { hs -= (uint32_t)kHS; hph ^= 1u; }
         float v[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = vn[e];
@@ -354,9 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
         if (warp == 0) TC_TRACE(pprof, 1, g);
         tc_after();
         if (!(a.dbg & 2)) {
-          const uint32_t col = tmem + lane_off + a_col0 + s * 64u + (uint32_t)hf * 16u;
+          const uint32_t col = tmem + lane_off + a_col0 + s * 32u;
           tmem_st16(col, hi);
-          tmem_st16(col + 32u, lo);
+          tmem_st16(col + 16u, lo);
           tmem_wait_st();
         }
         tc_before();
@@ -386,85 +395,89 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
         }
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ================= MMA issuer =================
-    // the whole warp runs the schedule (its ring state stays warp-uniform, in uniform
-    // registers); one elected lane issues each tcgen05.mma / commit
+  } else if (warp == kMmaWarp || warp == kMmaWarp + 1) {
+    // ================= MMA issuers =================
+    // Warp mw issues half hh = mw of every K chunk (k8 steps 2*mw, 2*mw + 1: 2 main + 4
+    // correction MMAs) from half-stage 2*g + mw.  Issuing blocks at the tensor pipe's
+    // rate (a shallow queue) and each commit / barrier wait stalls the issuing thread,
+    // so two issuers overlap one's commits and waits with the other's issue.  A turn
+    // barrier keeps the global issue order = (chunk, half) order, so the accumulation
+    // order is deterministic and unchanged per accumulator (main = hi*Bhi over k8;
+    // corr = lo*Bhi, hi*Blo over k8).  The pipe executes MMAs in issue order, so the
+    // group / tile commits (by the second-half issuer) cover both warps' MMAs.  Each
+    // warp runs the schedule warp-uniformly (uniform registers); an elected lane issues.
     {
+      const uint32_t mw = (uint32_t)(warp - kMmaWarp);
       // kind::tf32, D=F32, A/B = TF32, K-major, M = 128, N = BN
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
       const uint32_t d_corr = tmem + corr_col;
-      // Flat schedule over (tile, chunk).  A tile's correction MMAs wait for the previous
-      // tile's correction drain only after its main MMAs are queued, so the tile seam
-      // does not idle the tensor pipe.  Per accumulator the accumulation order is fixed:
-      // main = hi*Bhi over k8; corr = lo*Bhi, hi*Blo over k8.
       const int my_tiles = (int)blockIdx.x < ntile_total ? (ntile_total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
       const uint32_t total = (uint32_t)my_tiles * (uint32_t)a.nkc;
-      const bool mprof = (a.dbg & 64) && blockIdx.x == 0;
-      if (total) {
-        // ring positions advance incrementally: this is one thread's serial code, and a
-        // runtime division per chunk costs more than the barrier handshakes
-        uint32_t g = 0, gc = 0, tl = 0, sA = 0, phA = 0, sB = 0, phB = 0;
-        int kc = 0, kg = 0;
-        mbar_wait(fullB0, 0);
-        mbar_wait(fullA0, 0);
-        mbar_wait(acce0, 1u);
-        for (;;) {
-          const bool tile_end = kc == a.nkc - 1;
-          const bool grp_start = kg == 0;
-          const bool grp_end = tile_end || kg == a.G - 1;
-          const uint32_t acc = gc & 1u;
+      const bool mprof = (a.dbg & 64) && blockIdx.x == 0 && mw == 0;
+      // ring positions advance incrementally (no runtime divisions in this serial code)
+      uint32_t g = 0, gc = 0, tl = 0, hs = mw, hph = 0, sB = 0, phB = 0;
+      int kc = 0, kg = 0;
+      for (; g < total; ++g) {
+        const bool tile_end = kc == a.nkc - 1;
+        const bool grp_start = kg == 0;
+        const bool grp_end = tile_end || kg == a.G - 1;
+        const uint32_t acc = gc & 1u;
+        if (mw == 0) {
+          mbar_wait(fullB0 + 8 * sB, phB);
+          if (grp_start) mbar_wait(acce0 + 8 * acc, ((gc >> 1) & 1u) ^ 1u);
+        }
+        mbar_wait(fullA0 + 8 * hs, hph);
+        const uint32_t h = 2u * g + mw;
+        if (h) mbar_wait(turn, (h - 1u) & 1u);  // the previous half fully issued
+        tc_after();
+        TC_TRACE(mprof, 4, g);
+        const uint32_t d_tmem = tmem + acc * (uint32_t)BN;
+        const uint32_t a_hi = tmem + a_col0 + hs * 32u, a_lo = a_hi + 16u;
+        const uint32_t b_hi = sbase + sB * stage_bytes + mw * 64u, b_lo = b_hi + (uint32_t)BN * 128u;
+        if (!(a.dbg & 8) && elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            mma_tf32_ts(d_tmem, a_hi + k * 8u, desc_sw128(b_hi + k * 32u), idesc,
+                        (mw || !grp_start || k) ? 1u : 0u);
+        }
+        __syncwarp();
+        if (mw == 0 && kc == 0) {  // the previous tile's correction drain, after the main MMAs
+          mbar_wait(corre, (tl & 1u) ^ 1u);
           tc_after();
-          TC_TRACE(mprof, 4, g);
-          const uint32_t d_tmem = tmem + acc * (uint32_t)BN;
-          const uint32_t a_hi = tmem + a_col0 + sA * 64u, a_lo = a_hi + 32u;
-          const uint32_t b_hi = sbase + sB * stage_bytes, b_lo = b_hi + (uint32_t)BN * 128u;
-          if (!(a.dbg & 8) && elect_one()) {
+        }
+        if (elect_one()) {
+          if (!(a.dbg & 8)) {
 #pragma unroll
-            for (int k8 = 0; k8 < 4; ++k8)
-              mma_tf32_ts(d_tmem, a_hi + k8 * 8u, desc_sw128(b_hi + k8 * 32u), idesc, (!grp_start || k8) ? 1u : 0u);
-          }
-          __syncwarp();
-          if (kc == 0) {
-            mbar_wait(corre, (tl & 1u) ^ 1u);
-            tc_after();
-          }
-          if (elect_one()) {
-            if (!(a.dbg & 8)) {
-#pragma unroll
-              for (int k8 = 0; k8 < 4; ++k8) {
-                mma_tf32_ts(d_corr, a_lo + k8 * 8u, desc_sw128(b_hi + k8 * 32u), idesc, (kc || k8) ? 1u : 0u);
-                mma_tf32_ts(d_corr, a_hi + k8 * 8u, desc_sw128(b_lo + k8 * 32u), idesc, 1u);
-              }
+            for (int k = 0; k < 2; ++k) {
+              mma_tf32_ts(d_corr, a_lo + k * 8u, desc_sw128(b_hi + k * 32u), idesc, (mw || kc || k) ? 1u : 0u);
+              mma_tf32_ts(d_corr, a_hi + k * 8u, desc_sw128(b_lo + k * 32u), idesc, 1u);
             }
-            TC_TRACE(mprof, 5, g);
-            // release the stage first (the producers are on the critical path), then wait
-            // for the next chunk's operands / accumulator buffer
-            mma_commit(emptyA0 + 8 * sA);
+          }
+          mbar_arrive(turn);
+          TC_TRACE(mprof, 5, g);
+          mma_commit(emptyA0 + 8 * hs);
+          if (mw == 1) {
             mma_commit(emptyB0 + 8 * sB);
             if (grp_end) mma_commit(accf0 + 8 * acc);
             if (tile_end) mma_commit(corrf);
           }
-          __syncwarp();
-          if (++g == total) break;
-          if (++sA == (uint32_t)kSA) { sA = 0; phA ^= 1u; }
-          if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
-          mbar_wait(fullB0 + 8 * sB, phB);
-          mbar_wait(fullA0 + 8 * sA, phA);
-          if (grp_end) {
-            ++gc;
-            kg = 0;
-            mbar_wait(acce0 + 8 * (gc & 1u), ((gc >> 1) & 1u) ^ 1u);
-          } else {
-            ++kg;
-          }
-          if (tile_end) {
-            ++tl;
-            kc = 0;
-          } else {
-            ++kc;
-          }
+        }
+        __syncwarp();
+        hs += 2;
+        if (hs >= (uint32_t)kHS) { hs -= (uint32_t)kHS; hph ^= 1u; }
+        if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
+        if (grp_end) {
+          ++gc;
+          kg = 0;
+        } else {
+          ++kg;
+        }
+        if (tile_end) {
+          ++tl;
+          kc = 0;
+        } else {
+          ++kc;
         }
       }
     }
@@ -835,7 +848,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   // as many B stages as shared memory allows (2..8) after the tap table
   const size_t fixed = 1024 + (size_t)p->nkc * kBK * 8 + 512;
   int SB = (int)((227 * 1024 - fixed) / ((size_t)p->BN * 256));
-  SB = SB > 8 ? 8 : SB;
+  SB = SB > 4 ? 4 : SB;  // deeper B rings measured no faster and take L1 capacity
   if (SB < stages_host(p->BN)) {
     set_error(FTC_CONFIG_ERROR, "tcgen05 conv: shared memory too small for the B ring");
     return FTC_CONFIG_ERROR;

@@ -44,41 +44,6 @@ __global__ void k_act_pool(const float* __restrict__ in, float* __restrict__ out
   }
 }
 
-// act + pool for the whole batch at one (c, ox, oy): the thread walks n ascending,
-// writes out[n,c,ox,oy] (coalesced across threads) and accumulates the next layer's
-// input checksums exactly as input_checksums does (checksums.hpp:100-107).
-__global__ void k_act_pool_ck(const float* __restrict__ in, float* __restrict__ out, int N, int C,
-                              int H, int act, int k, int s, int p, int Ho, double* __restrict__ cd1,
-                              double* __restrict__ cd2) {
-  const long long plane = (long long)Ho * Ho;
-  const long long per = (long long)C * plane;
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= per) return;
-  const int oy = (int)(e % Ho), ox = (int)((e / Ho) % Ho), c = (int)(e / plane);
-  const long long in_per = (long long)C * H * H;
-  const float* src0 = in + (long long)c * H * H;
-  double s1 = 0.0, s2 = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const float* src = src0 + (long long)n * in_per;
-    float m = -INFINITY;
-    for (int i = 0; i < k; ++i) {
-      const int x = ox * s - p + i;
-      if (x < 0 || x >= H) continue;
-      for (int j = 0; j < k; ++j) {
-        const int y = oy * s - p + j;
-        if (y < 0 || y >= H) continue;
-        m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
-      }
-    }
-    out[(long long)n * per + e] = m;
-    const double v = (double)m;
-    s1 = __dadd_rn(s1, v);
-    s2 = __dadd_rn(s2, __dmul_rn((double)n, v));
-  }
-  cd1[e] = s1;
-  cd2[e] = s2;
-}
-
 __global__ void k_add_act(const float* __restrict__ a, const float* __restrict__ b,
                           float* __restrict__ out, long long n, int act) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -133,12 +98,16 @@ int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int3
     set_error(FTC_CONFIG_ERROR, "bad pooling window or null buffer");
     return FTC_CONFIG_ERROR;
   }
+  // act + pool over the whole batch in parallel, then the next layer's input checksums
+  // (exact reference order, n ascending) from the pooled tensor while it is L2-hot.
+  // (A fused per-(c,x,y) kernel walking n serially had too little parallelism: 25% of
+  // the AlexNet step.)
   const int Ho = (H + 2 * p - k) / s + 1;
   const long long per = (long long)C * Ho * Ho;
-  FTC_LAUNCH(k_act_pool_ck<<<(int)((per + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      in, out, N, C, H, act, k, s, p, Ho, cd1, cd2));
+  FTC_LAUNCH(k_act_pool<<<grid_for((long long)N * per), 256, 0, (cudaStream_t)stream>>>(
+      in, out, N * C, H, act, k, s, p, Ho));
   FTC_CUDA_CHECK(cudaGetLastError());
-  return FTC_OK;
+  return launch_input_checksums(out, N, per, cd1, cd2, (cudaStream_t)stream);
 }
 
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act, void* stream) {
