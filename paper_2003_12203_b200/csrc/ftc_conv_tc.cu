@@ -34,10 +34,12 @@
 // one takes a third of the updates.  Main accumulators are double-buffered in TMEM
 // so draining group g overlaps the MMAs of group g+1.  TMEM: [0, 2*BN) main,
 // [2*BN, 3*BN) correction, then 4-8 A half-stages of 32 columns (16 hi + 16 lo).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <string>
 #include <type_traits>
 
 #include "ftc_common.cuh"
@@ -53,7 +55,12 @@ struct TcPlan {
   float* Wp = nullptr;  // [ntiles][nkc][2][BN][32], SW128-swizzled, hi then lo
   int2* tab = nullptr;  // NCHW: [nkc*32] per-column taps {c*H*H + i*H + j, 1<<i | 1<<(16+j)}
                         // NHWC: [nkc] per-chunk taps {(i*H + j)*C + c0, same bits}
-  float* Dt = nullptr;  // NHWC copy of the input (N*H*H*C), nhwc only
+  float* Dt = nullptr;  // NHWC copy of the input (N*H*H*C), nhwc / im2col only
+  // TMA im2col A operand (C % 32 == 0): the tensor engine gathers each K chunk (one
+  // tap, 32 channels, 128 consecutive output pixels, zero-filled padding) from the NHWC
+  // copy straight into a swizzled shared-memory stage
+  bool im2col = false;
+  alignas(64) CUtensorMap tmA;
 };
 
 namespace {
@@ -67,6 +74,8 @@ constexpr int stages_for() {
   return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4);
 }
 constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
+constexpr int kAS = 4;                       // MODE 2 shared-memory A stages
+constexpr uint32_t kAStageBytes = 128u * 128u;  // 128 pixels x 32 FP32 channels
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
 constexpr int kLoaderWarp = 8;
 constexpr int kMmaWarp = 9;  // and 10: two issuers alternating K chunks
@@ -128,6 +137,17 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// im2col TMA: 128 consecutive output pixels (starting at input position (n, h, w) of the
+// bounding-box traversal) x channels [c, c+32) at filter tap (oh, ow)
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                              uint16_t ow, uint16_t oh, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(ow), "h"(oh)
+      : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t p;
   asm volatile(
@@ -222,8 +242,12 @@ __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int
   return h;
 }
 
-template <int BN, bool NHWC>
-__global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
+// MODE 0: NCHW im2col gather by the producers; 1: NHWC gather (4 x 16-byte loads per
+// chunk); 2: TMA im2col into shared memory, producers only split and store to TMEM
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_constant__ CUtensorMap tmA) {
+  constexpr bool NHWC = MODE == 1;
+  constexpr bool TMAA = MODE == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the B stages (SW128 atoms)
   const uint32_t raw = smem_u32(smem_raw);
@@ -235,10 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const int SB = a.SB;
   constexpr int kSA = stages_for<BN>();
   const uint32_t stage_bytes = (uint32_t)BN * 256u;  // hi + lo tiles, 128 B per row each
-  int2* tab_s = reinterpret_cast<int2*>(sptr + SB * stage_bytes);
-  const uint32_t tab_bytes = (uint32_t)a.nkc * kBK * 8u;
-  const uint32_t bar_base = sbase + SB * stage_bytes + tab_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + SB * stage_bytes + tab_bytes);
+  // MODE 2: kAS shared-memory A stages (128 pixels x 32 channels, SW128) follow the B ring
+  const uint32_t as_base = sbase + SB * stage_bytes;
+  const uint32_t as_bytes = TMAA ? (uint32_t)kAS * kAStageBytes : 0u;
+  int2* tab_s = reinterpret_cast<int2*>(sptr + SB * stage_bytes + as_bytes);
+  const uint32_t tab_bytes = TMAA ? 0u : (uint32_t)a.nkc * kBK * 8u;
+  const uint32_t bar_base = sbase + SB * stage_bytes + as_bytes + tab_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sptr + SB * stage_bytes + as_bytes + tab_bytes);
   // A ring of half-stages: a K chunk's first 16 columns (hf = 0) and last 16 (hf = 1)
   // are separate stages of 32 TMEM columns (16 hi + 16 lo), filled by their own producer
   // warps and released after their own 6 MMAs -- the refill of a stage overlaps 3 half
@@ -249,10 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
   const uint32_t fullB0 = bar_base + 8 * 16, emptyB0 = fullB0 + 8 * kMaxSB;
   const uint32_t accf0 = emptyB0 + 8 * kMaxSB, acce0 = accf0 + 16;
   const uint32_t corrf = acce0 + 16, corre = corrf + 8, turn = corre + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kMaxSB + 7);
+  const uint32_t fullAs0 = turn + 8, emptyAs0 = fullAs0 + 8 * kAS;  // MODE 2 A ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kMaxSB + 7 + 2 * kAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
+  if (!TMAA)
+    for (int e = threadIdx.x; e < a.nkc * kBK; e += blockDim.x) tab_s[e] = a.tab[e];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kHS; ++s) {
       mbar_init(fullA0 + 8 * s, kProdWarps / 2);
@@ -269,6 +298,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     mbar_init(corrf, 1);
     mbar_init(corre, kEpiThreads / 32);
     mbar_init(turn, 1);
+    if (TMAA) {  // shared-memory A ring: filled by the TMA, released by the producers
+      for (int s = 0; s < kAS; ++s) {
+        mbar_init(fullAs0 + 8 * s, 1);
+        mbar_init(emptyAs0 + 8 * s, kProdWarps);
+      }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kLoaderWarp) {
@@ -294,6 +329,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
     const int r = q * 32 + lane;  // row of the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t g = 0, hs = (uint32_t)hf, hph = 0;  // this warp's half-stage slot / phase
+    if constexpr (TMAA) {
+      // the chunk is already gathered (and zero-padded) by the TMA: read this row's 16
+      // values (4 x 16-byte chunks of the SW128 row, conflict-free), release the stage,
+      // split hi/lo and store them to the TMEM half-stage like the gather paths
+      uint32_t sa = 0, pha = 0;
+      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+        for (int kc = 0; kc < a.nkc; ++kc, ++g) {
+          const uint32_t s = hs, ph = hph;
+          hs += 2;
+          if (hs >= (uint32_t)kHS) { hs -= (uint32_t)kHS; hph ^= 1u; }
+          const uint32_t sa_c = sa, pha_c = pha;
+          if (++sa == (uint32_t)kAS) { sa = 0; pha ^= 1u; }
+          mbar_wait(fullAs0 + 8 * sa_c, pha_c);
+          const uint32_t row = as_base + sa_c * kAStageBytes + (uint32_t)r * 128u;
+          uint32_t v[16];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint32_t c = (uint32_t)(hf * 4 + q4);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[4 * q4]), "=r"(v[4 * q4 + 1]), "=r"(v[4 * q4 + 2]), "=r"(v[4 * q4 + 3])
+                         : "r"(row + ((c ^ (uint32_t)(r & 7)) << 4))
+                         : "memory");
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(emptyAs0 + 8 * sa_c);
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t h = (v[e] + 0x1000u) & 0xFFFFE000u;
+            hi[e] = h;
+            const float l = __uint_as_float(v[e]) - __uint_as_float(h);
+            lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
+          }
+          mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+          tc_after();
+          const uint32_t col = tmem + lane_off + a_col0 + s * 32u;
+          tmem_st16(col, hi);
+          tmem_st16(col + 16u, lo);
+          tmem_wait_st();
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(fullA0 + 8 * s);
+        }
+      }
+    } else {
     const bool pprof = (a.dbg & 64) && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kProdWarps - 1);
     for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
       const int pt = a.pt_lo + t % a.npt;
@@ -374,14 +454,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a) {
         TC_TRACE(pprof, warp == 0 ? 2 : 3, g);
       }
     }
+    }
   } else if (warp == kLoaderWarp) {
     // ================= B loader =================
     if (lane == 0) {
-      uint32_t g = 0, sB = 0, phB = 0;
+      uint32_t g = 0, sB = 0, phB = 0, sa = 0, pha = 0;
+      const int ncb = a.C / 32;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
         const int nt = t / a.npt;
         const float* src = a.Wp + (long long)nt * a.nkc * 2 * BN * kBK;
+        // MODE 2: the tile's first output pixel, as a TMA im2col traversal start
+        const long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
+        const int n0 = (int)(p0 / E2), f0 = (int)(p0 % E2);
+        const int cw = (f0 % E) * a.U - a.pad, ch = (f0 / E) * a.U - a.pad;
+        int ti = 0, tj = 0, cb = 0;  // K chunk kc = ((ti*R + tj)*ncb + cb)
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
+          if constexpr (TMAA) {
+            mbar_wait(emptyAs0 + 8 * sa, pha ^ 1u);
+            if (a.dbg & 1) {  // profiling: skip the A gather
+              mbar_arrive(fullAs0 + 8 * sa);
+            } else {
+              mbar_arrive_expect_tx(fullAs0 + 8 * sa, kAStageBytes);
+              tma_im2col_4d(as_base + sa * kAStageBytes, &tmA, cb * 32, cw, ch, n0, (uint16_t)tj, (uint16_t)ti,
+                            fullAs0 + 8 * sa);
+            }
+            if (++sa == (uint32_t)kAS) { sa = 0; pha ^= 1u; }
+            if (++cb == ncb) {
+              cb = 0;
+              if (++tj == R) { tj = 0; ++ti; }
+            }
+          }
           const uint32_t s = sB, ph = phB;
           if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
           mbar_wait(emptyB0 + 8 * s, ph ^ 1u);
@@ -702,15 +804,15 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
 
 int g_num_sms = 0;
 
-template <int BN, bool NHWC>
-int launch_bn(const TcArgs& a, int grid, size_t smem, cudaStream_t s) {
+template <int BN, int MODE>
+int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, NHWC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     attr_set = true;
   }
-  FTC_LAUNCH(k_conv_tc<BN, NHWC><<<grid, kThreads, smem, s>>>(a));
+  FTC_LAUNCH(k_conv_tc<BN, MODE><<<grid, kThreads, smem, s>>>(a, tm));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -749,7 +851,10 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
   }
   // channel-last gather: faster producers, but with the MMA issue chain the bottleneck it
   // does not pay for its transpose pass yet (AlexNet conv2 669 vs 641 us): opt-in
-  p->nhwc = d.C % 32 == 0 && getenv("FTC_TC_NHWC") != nullptr;
+  // K order: tap-major (k = (i*R + j)*C + c) for the channel-last paths
+  const bool corners_ok = d.pad <= 127 && d.pad - (d.R - 1) >= -128 && d.stride <= 8;
+  p->im2col = d.C % 32 == 0 && corners_ok && !getenv("FTC_TC_NO_TMA") && !getenv("FTC_TC_NHWC");
+  p->nhwc = !p->im2col && d.C % 32 == 0 && getenv("FTC_TC_NHWC") != nullptr;
   if (const char* bn = getenv("FTC_TC_MAX_BN")) {  // experimentation: cap the N tile
     const int cap = atoi(bn);
     if ((cap == 32 || cap == 64 || cap == 96 || cap == 128) && p->BN > cap) {
@@ -764,14 +869,42 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
     return FTC_CUDA_ERROR;
   }
   FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, d.M, p->K, p->BN, p->ntiles, p->nkc, d.C, d.R * d.R,
-                                         p->nhwc ? 1 : 0));
+                                         (p->nhwc || p->im2col) ? 1 : 0));
   if (cudaMalloc(&p->tab, (size_t)p->nkc * kBK * sizeof(int2)) != cudaSuccess) {
     cudaFree(p->Wp);
     delete p;
     set_error(FTC_CUDA_ERROR, "cudaMalloc(tap table) failed");
     return FTC_CUDA_ERROR;
   }
-  if (p->nhwc) {
+  if (p->im2col) {
+    if (cudaMalloc(&p->Dt, (size_t)d.N * d.C * d.H * d.H * sizeof(float)) != cudaSuccess) {
+      cudaFree(p->Wp);
+      cudaFree(p->tab);
+      delete p;
+      set_error(FTC_CUDA_ERROR, "cudaMalloc(NHWC input copy) failed");
+      return FTC_CUDA_ERROR;
+    }
+    // NHWC tensor {C, W, H, N}; the traversal box spans the output positions' window
+    // origins (lower corner -pad, upper corner pad - (R-1)) with stride U
+    const cuuint64_t dims[4] = {(cuuint64_t)d.C, (cuuint64_t)d.H, (cuuint64_t)d.H, (cuuint64_t)d.N};
+    const cuuint64_t strides[3] = {(cuuint64_t)d.C * 4, (cuuint64_t)d.C * d.H * 4,
+                                   (cuuint64_t)d.C * d.H * d.H * 4};
+    const int lower[2] = {-d.pad, -d.pad};
+    const int upper[2] = {d.pad - (d.R - 1), d.pad - (d.R - 1)};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)d.stride, (cuuint32_t)d.stride, 1};
+    const CUresult cr = cuTensorMapEncodeIm2col(&p->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p->Dt, dims, strides,
+                                                lower, upper, 32, 128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+      cudaFree(p->Wp);
+      cudaFree(p->tab);
+      cudaFree(p->Dt);
+      delete p;
+      set_error(FTC_CUDA_ERROR, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)cr) + ")");
+      return FTC_CUDA_ERROR;
+    }
+  } else if (p->nhwc) {
     cudaMemsetAsync(p->tab, 0, (size_t)p->nkc * kBK * sizeof(int2), s);
     FTC_LAUNCH(k_build_tab_nhwc<<<(p->nkc + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->nkc));
     if (cudaMalloc(&p->Dt, (size_t)d.N * d.C * d.H * d.H * sizeof(float)) != cudaSuccess) {
@@ -846,7 +979,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   const int tiles = a.ntiles * a.npt;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   // as many B stages as shared memory allows (2..8) after the tap table
-  const size_t fixed = 1024 + (size_t)p->nkc * kBK * 8 + 512;
+  const size_t fixed = p->im2col ? 1024 + (size_t)kAS * kAStageBytes + 512 : 1024 + (size_t)p->nkc * kBK * 8 + 512;
   int SB = (int)((227 * 1024 - fixed) / ((size_t)p->BN * 256));
   SB = SB > 4 ? 4 : SB;  // deeper B rings measured no faster and take L1 capacity
   if (SB < stages_host(p->BN)) {
@@ -860,23 +993,32 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   a.SB = SB;
   a.dbg = getenv("FTC_TC_DEBUG") ? atoi(getenv("FTC_TC_DEBUG")) : 0;
   const size_t smem = fixed + (size_t)SB * p->BN * 256;
-  if (p->nhwc) {
+  if (p->nhwc || p->im2col) {
     const int nimg = c.img_hi - c.img_lo;
     const dim3 tg((unsigned)((c.H * c.H + 31) / 32), (unsigned)(c.C / 32), (unsigned)nimg);
     FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(c.D, p->Dt, c.C, c.H * c.H, c.img_lo));
     a.D = p->Dt;
+  }
+  if (p->im2col) {
     switch (p->BN) {
-      case 32: return launch_bn<32, true>(a, grid, smem, s);
-      case 64: return launch_bn<64, true>(a, grid, smem, s);
-      case 96: return launch_bn<96, true>(a, grid, smem, s);
-      case 128: return launch_bn<128, true>(a, grid, smem, s);
+      case 32: return launch_bn<32, 2>(a, p->tmA, grid, smem, s);
+      case 64: return launch_bn<64, 2>(a, p->tmA, grid, smem, s);
+      case 96: return launch_bn<96, 2>(a, p->tmA, grid, smem, s);
+      case 128: return launch_bn<128, 2>(a, p->tmA, grid, smem, s);
+    }
+  } else if (p->nhwc) {
+    switch (p->BN) {
+      case 32: return launch_bn<32, 1>(a, p->tmA, grid, smem, s);
+      case 64: return launch_bn<64, 1>(a, p->tmA, grid, smem, s);
+      case 96: return launch_bn<96, 1>(a, p->tmA, grid, smem, s);
+      case 128: return launch_bn<128, 1>(a, p->tmA, grid, smem, s);
     }
   } else {
     switch (p->BN) {
-      case 32: return launch_bn<32, false>(a, grid, smem, s);
-      case 64: return launch_bn<64, false>(a, grid, smem, s);
-      case 96: return launch_bn<96, false>(a, grid, smem, s);
-      case 128: return launch_bn<128, false>(a, grid, smem, s);
+      case 32: return launch_bn<32, 0>(a, p->tmA, grid, smem, s);
+      case 64: return launch_bn<64, 0>(a, p->tmA, grid, smem, s);
+      case 96: return launch_bn<96, 0>(a, p->tmA, grid, smem, s);
+      case 128: return launch_bn<128, 0>(a, p->tmA, grid, smem, s);
     }
   }
   set_error(FTC_CONFIG_ERROR, "unsupported BN");
