@@ -591,6 +591,13 @@ int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N
 
 int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
                       int pad, int E, cudaStream_t s) {
+  static bool carve = false;
+  if (!carve && getenv("FTC_CARVEOUT")) {
+    cudaFuncSetAttribute(k_co5_sliced<3>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_co5_sliced<5>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_co5_sliced<0>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   const int g = (E * E + 31) / 32, t = 32 * kDetSlices;
   switch (R) {
     case 1: FTC_LAUNCH(k_co5_sliced<1><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
@@ -606,6 +613,12 @@ int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, 
 int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                       const double* agg, double tau, DetectStats* st, unsigned int* ticket,
                       DetectStats* host_out, cudaStream_t s) {
+  static bool carve = false;
+  if (!carve && getenv("FTC_CARVEOUT")) {  // experiment: keep the conv's L1/SMEM split
+    cudaFuncSetAttribute(k_detect_so5, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   FTC_LAUNCH(k_detect_so5<<<(E2 + 31) / 32, 32 * kDetSlices, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg,
                                                                       tau, st, ticket, host_out));
   FTC_CUDA_CHECK(cudaGetLastError());

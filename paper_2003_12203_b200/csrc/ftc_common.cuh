@@ -90,6 +90,26 @@ __device__ __forceinline__ float apply_output_faults(float v, int n, int m, int 
 }
 
 // ------------------------------------------------------------------ conv engine
+struct DetectStats {
+  int32_t flagged;
+  int32_t pad_;
+  unsigned long long max_rel_dev_bits;
+};
+
+// Clean-path CoC-D fused into the tcgen05 conv (TMA im2col engine): Co5 = Cd1 (x) Cw1 is
+// computed before the conv; the conv adds its pixels' row sums into So5 (FP64 atomics)
+// and its last CTA compares them and publishes the record.
+struct FusedDetect {
+  double* co5;            // [E2], computed before the conv
+  double* so5;            // [E2] accumulator: zero on entry, re-zeroed by the last CTA
+  const double* agg;      // bias aggregates (agg[0] = sum_m B[m])
+  double tau;
+  int bias;
+  DetectStats* st;        // device counters, zero on entry, re-zeroed
+  unsigned int* ticket;   // zero on entry, re-zeroed
+  DetectStats* host_out;  // mapped host record
+};
+
 struct ConvArgs {
   const float* D;  // N x C x H x H
   const float* W;  // M x Ckw x R x R (reference layout)
@@ -102,6 +122,8 @@ struct ConvArgs {
   double* rowsum_m;  // [N][E2] sum_m m*O (So4 before bias adjust), may be null
   const uint32_t* plane_mask;  // N*M bits: store only these planes (repair); null = all
   int img_lo, img_hi;          // images to compute
+  const FusedDetect* fd;       // tcgen05 im2col engine only; null = detection runs outside
+  bool dt_ready;               // tcgen05 im2col/NHWC engine: the NHWC copy is already filled
 };
 
 int conv_simt_launch(const ConvArgs& a, cudaStream_t s);
@@ -112,7 +134,13 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
 void tc_plan_destroy(TcPlan* p);
 bool tc_supported(const ftc_conv_desc& d);
 int conv_tc_launch(const TcPlan* p, const ConvArgs& a, cudaStream_t s);
-int tc_rowsum_parts(const TcPlan* p);  // N-tiles = row-sum partial slabs of N*E2
+int tc_rowsum_parts(const TcPlan* p);
+bool tc_im2col(const TcPlan* p);           // TMA im2col engine (fused detection available)
+float* tc_nhwc_buffer(const TcPlan* p);    // its NHWC input copy
+// D (NCHW) -> Dt (NHWC) for images [n_lo, n_lo + nimg); with cd1 != null also the exact
+// input checksums Cd1/Cd2 (n ascending, FP64; whole batch only: n_lo = 0, nimg = N)
+int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg, double* cd1, double* cd2,
+                   cudaStream_t s);  // N-tiles = row-sum partial slabs of N*E2
 
 // ------------------------------------------------------------------ checksum kernels
 // input_checksums (exact order)
@@ -142,11 +170,6 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
                              const float* bias, const double* agg, double* const so[7],
                              cudaStream_t s);
 // clean-path CoC-D: so5 = sum_n rowsum (bias adjusted) vs co5; stats into dev[0..]
-struct DetectStats {
-  int32_t flagged;
-  int32_t pad_;
-  unsigned long long max_rel_dev_bits;
-};
 int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                        const double* agg, double tau, DetectStats* st, cudaStream_t s);
 // clean path: Cd1 only, parallel over positions (FTC_CONFIG_ERROR when the plane size

@@ -100,6 +100,8 @@ struct TcArgs {
   double* rowsum;    // [2*ntiles][N*E2] or null (one slab per column half)
   double* rowsum_m;  // [2*ntiles][N*E2]
   const uint32_t* plane_mask;
+  FusedDetect fd;  // valid when fuse != 0 (MODE 2)
+  int fuse;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -717,7 +719,78 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         a.rowsum[o] = rs;
         a.rowsum_m[o] = rsm;
       }
+      // fused CoC-D: So5 accumulates from the row sums (order-free FP64 atomics; the exact
+      // families are recomputed in reference order if anything is flagged)
+      if (TMAA && a.fuse && valid) atomicAdd(a.fd.so5 + f, rs);
       TC_TRACE(eprof, 9, tl);
+    }
+    if (TMAA && a.fuse) {
+      // fused CoC-D: the last CTA to finish compares So5 (bias adjusted) with Co5
+      // at every position (values_differ), publishes {flagged, max_rel_dev} into the
+      // mapped host record and re-zeroes So5 / counters / ticket for the next launch
+      volatile int& s_last = *reinterpret_cast<volatile int*>(tmem_slot + 1);  // dynamic smem
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      const int et = (int)threadIdx.x - kEpiWarp0 * 32;
+      if (et == 0) {
+        if (!(a.dbg & 2048)) __threadfence();
+        s_last = atomicAdd(a.fd.ticket, 1u) == gridDim.x - 1;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (s_last) {
+        __threadfence();
+        int bad = 0;
+        unsigned long long devb = 0ull;
+        for (int fb = et; fb < E2; fb += kEpiThreads * 8) {  // 8 positions' loads in flight
+          double sv[8], cv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int fp = fb + u * kEpiThreads;
+            sv[u] = fp < E2 ? __ldcg(a.fd.so5 + fp) : 0.0;
+            cv[u] = fp < E2 ? __ldcg(a.fd.co5 + fp) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int fp = fb + u * kEpiThreads;
+            if (fp >= E2) break;
+            a.fd.so5[fp] = 0.0;
+            double ss = sv[u];
+            if (a.fd.bias) ss -= (double)a.N * a.fd.agg[0];
+            const double c = cv[u];
+            double den = fabs(c);
+            if (den < fabs(ss)) den = fabs(ss);
+            if (den < 1.0) den = 1.0;
+            const double dev = fabs(c - ss) / den;
+            if (dev == dev && dev > 0.0) {
+              const unsigned long long b = (unsigned long long)__double_as_longlong(dev);
+              devb = b > devb ? b : devb;
+            }
+            bad += values_differ(c, ss, a.fd.tau) ? 1 : 0;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          bad += __shfl_xor_sync(0xffffffffu, bad, o);
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+          devb = other > devb ? other : devb;
+        }
+        if (lane == 0) {
+          if (bad) atomicAdd(&a.fd.st->flagged, bad);
+          if (devb) atomicMax(&a.fd.st->max_rel_dev_bits, devb);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (et == 0) {
+          __threadfence();
+          const int fl = atomicExch(&a.fd.st->flagged, 0);
+          const unsigned long long mb = atomicExch(&a.fd.st->max_rel_dev_bits, 0ull);
+          if (!(a.dbg & 1024)) {
+            volatile DetectStats* h = a.fd.host_out;
+            h->flagged = fl;
+            h->max_rel_dev_bits = mb;
+            __threadfence_system();
+          }
+          *a.fd.ticket = 0u;
+        }
+      }
     }
   }
   tc_before();
@@ -799,6 +872,44 @@ __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ 
   for (int r = threadIdx.y; r < 32; r += 8) {
     const int hw = hw0 + r, c = c0 + threadIdx.x;
     if (c < C && hw < HW) dst[(long long)hw * C + c] = t[threadIdx.x][r];
+  }
+}
+
+// D (NCHW) -> Dt (NHWC) and, optionally, the exact input checksums: a block owns a
+// 32-channel x 8-position tile for every image; each thread accumulates its own (c, hw)
+// over n ascending in FP64 (checksums.hpp:100-107 order), 8 images' loads in flight.
+__global__ void __launch_bounds__(256) k_nhwc_cd(const float* __restrict__ D, float* __restrict__ Dt, int C,
+                                                int HW, int n_lo, int nimg, double* __restrict__ cd1,
+                                                double* __restrict__ cd2) {
+  __shared__ float t[8][33];
+  const int tid = threadIdx.x;
+  const int cl = tid >> 3, hl = tid & 7;  // load: a warp reads 4 channel rows x 8 positions
+  const int c = blockIdx.y * 32 + cl, hw = blockIdx.x * 8 + hl;
+  const bool ok = hw < HW;
+  const int wc = tid & 31, wh = tid >> 5;  // store: a warp writes one position's 32 channels
+  const int sc = blockIdx.y * 32 + wc, shw = blockIdx.x * 8 + wh;
+  double s1 = 0.0, s2 = 0.0;
+  for (int b = 0; b < nimg; b += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = (ok && b + u < nimg) ? __ldg(D + ((long long)(n_lo + b + u) * C + c) * HW + hw) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (b + u >= nimg) break;
+      if (cd1) {
+        s1 = dadd(s1, (double)v[u]);
+        s2 = dadd(s2, dmul((double)(n_lo + b + u), (double)v[u]));
+      }
+      t[hl][cl] = v[u];
+      __syncthreads();
+      if (shw < HW) Dt[((long long)(n_lo + b + u) * HW + shw) * C + sc] = t[wh][wc];
+      __syncthreads();
+    }
+  }
+  if (cd1 && ok) {
+    cd1[(long long)c * HW + hw] = s1;
+    cd2[(long long)c * HW + hw] = s2;
   }
 }
 
@@ -938,6 +1049,25 @@ void tc_plan_destroy(TcPlan* p) {
 }
 
 int tc_rowsum_parts(const TcPlan* p) { return p ? 2 * p->ntiles : 1; }
+bool tc_im2col(const TcPlan* p) { return p && p->im2col; }
+float* tc_nhwc_buffer(const TcPlan* p) { return p ? p->Dt : nullptr; }
+
+int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg, double* cd1, double* cd2,
+                   cudaStream_t s) {
+  if (C % 32) {
+    set_error(FTC_CONFIG_ERROR, "launch_nhwc_cd: C % 32 != 0");
+    return FTC_CONFIG_ERROR;
+  }
+  static bool carve = false;
+  if (!carve && getenv("FTC_CARVEOUT")) {
+    cudaFuncSetAttribute(k_nhwc_cd, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
+  const dim3 g((unsigned)((HW + 7) / 8), (unsigned)(C / 32));
+  FTC_LAUNCH(k_nhwc_cd<<<g, 256, 0, s>>>(D, Dt, C, HW, n_lo, nimg, cd1, cd2));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
 
 int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   TcArgs a{};
@@ -994,10 +1124,20 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   a.dbg = getenv("FTC_TC_DEBUG") ? atoi(getenv("FTC_TC_DEBUG")) : 0;
   const size_t smem = fixed + (size_t)SB * p->BN * 256;
   if (p->nhwc || p->im2col) {
-    const int nimg = c.img_hi - c.img_lo;
-    const dim3 tg((unsigned)((c.H * c.H + 31) / 32), (unsigned)(c.C / 32), (unsigned)nimg);
-    FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(c.D, p->Dt, c.C, c.H * c.H, c.img_lo));
+    if (!c.dt_ready) {
+      const int st = launch_nhwc_cd(c.D, p->Dt, c.C, c.H * c.H, c.img_lo, c.img_hi - c.img_lo, nullptr, nullptr, s);
+      if (st != FTC_OK) return st;
+    }
     a.D = p->Dt;
+  }
+  a.fuse = 0;
+  if (c.fd) {
+    if (!p->im2col) {
+      set_error(FTC_CONFIG_ERROR, "fused detection needs the im2col engine");
+      return FTC_CONFIG_ERROR;
+    }
+    a.fd = *c.fd;
+    a.fuse = 1;
   }
   if (p->im2col) {
     switch (p->BN) {

@@ -63,6 +63,7 @@ struct ftc_layer {
   double *cw1w = nullptr, *cw2w = nullptr;  // working kernel checksums
   double *cd1 = nullptr, *cd2 = nullptr;
   double* co5f = nullptr;
+  double* so5acc = nullptr;  // fused clean path: So5 accumulator (zero between calls)
   double *rowsum = nullptr, *rowsum_m = nullptr;
   DetectStats* stats = nullptr;
   DetectStats* stats_h = nullptr;  // pinned
@@ -139,8 +140,11 @@ int dalloc(T** p, size_t count) {
 bool use_tc(const ftc_layer* L) { return g_engine == 0 && L->tc != nullptr; }
 
 int run_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults, bool sums,
-             const uint32_t* plane_mask, int img_lo, int img_hi, cudaStream_t s) {
+             const uint32_t* plane_mask, int img_lo, int img_hi, cudaStream_t s,
+             const FusedDetect* fd = nullptr, bool dt_ready = false) {
   ConvArgs a{};
+  a.fd = fd;
+  a.dt_ready = dt_ready;
   a.D = D;
   a.W = W;
   a.bias = L->d.bias_enabled ? L->bias : nullptr;
@@ -174,7 +178,7 @@ int run_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults
 
 // conv with optional event bracketing (bench.py's per-kernel roofline timing)
 int timed_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults, bool sums,
-               cudaStream_t s) {
+               cudaStream_t s, const FusedDetect* fd = nullptr, bool dt_ready = false) {
   if (L->timing) {
     if (L->conv_timed_pending) {  // harvest the previous bracket first
       FTC_CUDA_CHECK(cudaEventSynchronize(L->ev_c1));
@@ -186,7 +190,7 @@ int timed_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faul
     }
     FTC_CUDA_CHECK(cudaEventRecord(L->ev_c0, s));
   }
-  int st = run_conv(L, D, W, O, faults, sums, nullptr, 0, L->d.N, s);
+  int st = run_conv(L, D, W, O, faults, sums, nullptr, 0, L->d.N, s, fd, dt_ready);
   if (L->timing && st == FTC_OK) {
     FTC_CUDA_CHECK(cudaEventRecord(L->ev_c1, s));
     L->conv_timed_pending = true;
@@ -252,7 +256,7 @@ void free_layer(ftc_layer* L) {
     if (p) cudaFree(p);
   };
   F(L->W); F(L->W_work); F(L->bias); F(L->agg); F(L->cw1g); F(L->cw2g); F(L->cw1w); F(L->cw2w);
-  F(L->cd1); F(L->cd2); F(L->co5f); F(L->rowsum); F(L->rowsum_m); F(L->stats); F(L->faults_dev);
+  F(L->cd1); F(L->cd2); F(L->co5f); F(L->so5acc); F(L->rowsum); F(L->rowsum_m); F(L->stats); F(L->faults_dev);
   F(L->D_work); F(L->D_host_buf); F(L->O_host_buf);
   for (int k = 0; k < 7; ++k) {
     F(L->cs[k]);
@@ -720,8 +724,9 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
       (st = dalloc(&L->cw2g, L->nCw)) || (st = dalloc(&L->cw1w, L->nCw)) ||
       (st = dalloc(&L->cw2w, L->nCw)) || (st = dalloc(&L->cd1, L->nCd)) ||
       (st = dalloc(&L->cd2, L->nCd)) || (st = dalloc(&L->co5f, L->E2)) ||
-      (st = dalloc(&L->stats, 1)))
+      (st = dalloc(&L->so5acc, L->E2)) || (st = dalloc(&L->stats, 1)))
     return fail(st);
+  if (cudaMemset(L->so5acc, 0, L->E2 * sizeof(double)) != cudaSuccess) return fail(FTC_CUDA_ERROR);
   if (cudaMallocHost((void**)&L->stats_h, sizeof(DetectStats)) != cudaSuccess)
     return fail(FTC_CUDA_ERROR);
   if ((st = dalloc(&L->fstats, 1)) || (st = dalloc(&L->fticket, 1))) return fail(st);
@@ -869,6 +874,32 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
                                     has_target(faults, n_faults, FTC_FAULT_CD2));
   const double* cd1_use = L->cd1;
   L->cd_ext1 = L->cd_ext2 = nullptr;
+  const bool pre_faults = L->Dconv != D || L->Wcur != L->W || cwf || L->has_cd_faults;
+  // opt-in until it beats the side-stream path end to end (three dependent launches
+  // before the persistent conv cost more than the fusion saves)
+  static const bool fused_ok = getenv("FTC_FUSED_DETECT") != nullptr;
+  if (fused_ok && use_tc(L) && tc_im2col(L->tc) && !pre_faults) {
+    // Fused clean path (TMA im2col engine): one pre-pass writes the NHWC copy and, unless
+    // the producer of D already reduced it, the exact Cd1/Cd2; Co5 follows; the conv
+    // accumulates So5 from its row sums and its last CTA runs CoC-D -- no side stream,
+    // nothing launched after the persistent conv.
+    if (cd1_in) {
+      L->cd_ext1 = cd1_in;
+      L->cd_ext2 = cd2_in;
+      cd1_use = cd1_in;
+      CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, nullptr, nullptr, s));
+    } else {
+      CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s));
+    }
+    L->ck_exact = true;
+    CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, s));
+    FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
+                   L->fstats_hd};
+    CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, true, s, &fd, true));
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
+    L->inflight = true;
+    return FTC_OK;
+  }
   // The conv is enqueued first so its persistent CTAs are dispatched before the
   // side-stream checksum work, which then fills the SM resources they leave free.
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
