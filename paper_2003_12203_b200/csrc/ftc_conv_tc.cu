@@ -35,6 +35,7 @@
 // so draining group g overlaps the MMAs of group g+1.  TMEM: [0, 2*BN) main,
 // [2*BN, 3*BN) correction, then 4-8 A half-stages of 32 columns (16 hi + 16 lo).
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -1003,7 +1004,17 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
     const int lower[2] = {-d.pad, -d.pad};
     const int upper[2] = {d.pad - (d.R - 1), d.pad - (d.R - 1)};
     const cuuint32_t estr[4] = {1, (cuuint32_t)d.stride, (cuuint32_t)d.stride, 1};
-    const CUresult cr = cuTensorMapEncodeIm2col(&p->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p->Dt, dims, strides,
+    // driver entry point resolved at run time: the library carries no link-time
+    // dependency on libcuda (it must load on driverless build hosts)
+    static PFN_cuTensorMapEncodeIm2col_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                  &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        encode = nullptr;
+    }
+    const CUresult cr = !encode ? CUDA_ERROR_NOT_FOUND : encode(&p->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p->Dt, dims, strides,
                                                 lower, upper, 32, 128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
