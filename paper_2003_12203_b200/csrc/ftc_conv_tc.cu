@@ -250,7 +250,8 @@ __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_constant__ CUtensorMap tmA) {
   constexpr bool NHWC = MODE == 1;
-  constexpr bool TMAA = MODE == 2;
+  constexpr bool TMAA = MODE >= 2;
+  constexpr bool FUSE = MODE == 3;  // TMA im2col + fused clean-path CoC-D
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the B stages (SW128 atoms)
   const uint32_t raw = smem_u32(smem_raw);
@@ -722,10 +723,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       }
       // fused CoC-D: So5 accumulates from the row sums (order-free FP64 atomics; the exact
       // families are recomputed in reference order if anything is flagged)
-      if (TMAA && a.fuse && valid) atomicAdd(a.fd.so5 + f, rs);
+      if (FUSE && valid) atomicAdd(a.fd.so5 + f, rs);
       TC_TRACE(eprof, 9, tl);
     }
-    if (TMAA && a.fuse) {
+    if constexpr (FUSE) {
       // fused CoC-D: the last CTA to finish compares So5 (bias adjusted) with Co5
       // at every position (values_differ), publishes {flagged, max_rel_dev} into the
       // mapped host record and re-zeroes So5 / counters / ticket for the next launch
@@ -1074,6 +1075,12 @@ int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg,
     cudaFuncSetAttribute(k_nhwc_cd, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     carve = true;
   }
+  if (!cd1) {  // transpose only: parallel over images too
+    const dim3 tg((unsigned)((HW + 31) / 32), (unsigned)(C / 32), (unsigned)nimg);
+    FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(D, Dt, C, HW, n_lo));
+    FTC_CUDA_CHECK(cudaGetLastError());
+    return FTC_OK;
+  }
   const dim3 g((unsigned)((HW + 7) / 8), (unsigned)(C / 32));
   FTC_LAUNCH(k_nhwc_cd<<<g, 256, 0, s>>>(D, Dt, C, HW, n_lo, nimg, cd1, cd2));
   FTC_CUDA_CHECK(cudaGetLastError());
@@ -1150,7 +1157,14 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
     a.fd = *c.fd;
     a.fuse = 1;
   }
-  if (p->im2col) {
+  if (p->im2col && a.fuse) {
+    switch (p->BN) {
+      case 32: return launch_bn<32, 3>(a, p->tmA, grid, smem, s);
+      case 64: return launch_bn<64, 3>(a, p->tmA, grid, smem, s);
+      case 96: return launch_bn<96, 3>(a, p->tmA, grid, smem, s);
+      case 128: return launch_bn<128, 3>(a, p->tmA, grid, smem, s);
+    }
+  } else if (p->im2col) {
     switch (p->BN) {
       case 32: return launch_bn<32, 2>(a, p->tmA, grid, smem, s);
       case 64: return launch_bn<64, 2>(a, p->tmA, grid, smem, s);
