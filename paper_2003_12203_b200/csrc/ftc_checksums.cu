@@ -486,6 +486,129 @@ __global__ void __launch_bounds__(32 * kDetSlices) k_detect_so5(
   }
 }
 
+// Adaptive forms for the clean path: a 256-thread block covers P positions x S slices
+// (S = 256 / P) so a layer with few positions still fills the GPU and each thread does
+// only a few channels (Co5) or batch terms (So5) -- the fixed 32-position blocks left
+// 13x13 layers on 6 blocks with 24-48 serial steps per thread.
+template <int RT>
+__global__ void __launch_bounds__(256) k_co5_adapt(const double* __restrict__ cd1, const double* __restrict__ cw1,
+                                                  double* __restrict__ co5, int C, int H, int Rrt, int U, int pad,
+                                                  int E, int P) {
+  __shared__ double red[256];
+  const int R = RT > 0 ? RT : Rrt, RR = R * R, E2 = E * E, S = 256 / P;
+  const int t = threadIdx.x, pl = t % P, sl = t / P;
+  const int f = blockIdx.x * P + pl;
+  double c5 = 0.0;
+  if (f < E2) {
+    const int x = f / E, y = f - (f / E) * E;
+    const int hb = x * U - pad, wb = y * U - pad;
+    for (int c = sl; c < C; c += S) {
+      const double* src = cd1 + (long long)c * H * H;
+      const double* ker = cw1 + c * RR;
+      if constexpr (RT > 0) {
+        double v[RT * RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+          for (int j = 0; j < RT; ++j) {
+            const bool ok = (unsigned)(hb + i) < (unsigned)H && (unsigned)(wb + j) < (unsigned)H;
+            v[i * RT + j] = ok ? __ldg(src + (hb + i) * H + wb + j) : 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < RT * RT; ++q) c5 = fma(v[q], __ldg(ker + q), c5);
+      } else {
+        for (int i = 0; i < R; ++i) {
+          const int hh = hb + i;
+          if (hh < 0 || hh >= H) continue;
+          for (int j = 0; j < R; ++j) {
+            const int ww = wb + j;
+            if (ww < 0 || ww >= H) continue;
+            c5 = fma(__ldg(src + hh * H + ww), __ldg(ker + i * R + j), c5);
+          }
+        }
+      }
+    }
+  }
+  red[t] = c5;
+  __syncthreads();
+  if (t < P && f < E2) {
+    double cc = 0.0;
+    for (int q = 0; q < S; ++q) cc += red[q * P + t];
+    co5[f] = cc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_detect_adapt(const double* __restrict__ co5,
+                                                     const double* __restrict__ rowsum, int parts, int N, int E2,
+                                                     int bias, const double* agg, double tau, DetectStats* st,
+                                                     unsigned int* ticket, DetectStats* host_out, int P) {
+  __shared__ double red[256];
+  const int S = 256 / P;
+  const int t = threadIdx.x, pl = t % P, sl = t / P;
+  const int f = blockIdx.x * P + pl;
+  double s5 = 0.0;
+  if (f < E2) {
+    const long long slab = (long long)N * E2;
+    const int terms = N * parts;
+    for (int q = sl; q < terms; q += S) {
+      const int sq = q / N, n = q - sq * N;
+      s5 += __ldg(rowsum + sq * slab + (long long)n * E2 + f);
+    }
+  }
+  red[t] = s5;
+  __syncthreads();
+  if (t < 32) {
+    int bad = 0;
+    unsigned long long devb = 0ull;
+    for (int pp = t; pp < P; pp += 32) {
+      const int ff = blockIdx.x * P + pp;
+      if (ff >= E2) continue;
+      double ss = 0.0;
+      for (int q = 0; q < S; ++q) ss += red[q * P + pp];
+      if (bias) ss -= (double)N * agg[0];
+      const double c = co5[ff];
+      double den = fabs(c);
+      if (den < fabs(ss)) den = fabs(ss);
+      if (den < 1.0) den = 1.0;
+      const double dev = fabs(c - ss) / den;
+      if (dev == dev && dev > 0.0) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(dev);
+        devb = b > devb ? b : devb;
+      }
+      bad += values_differ(c, ss, tau) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+      devb = other > devb ? other : devb;
+    }
+    if (t == 0) {
+      if (bad) atomicAdd(&st->flagged, bad);
+      if (devb) atomicMax(&st->max_rel_dev_bits, devb);
+      __threadfence();
+      const unsigned int done = atomicAdd(ticket, 1u);
+      if (done == gridDim.x - 1) {  // last block: publish and reset
+        __threadfence();
+        const int fl = atomicExch(&st->flagged, 0);
+        const unsigned long long mb = atomicExch(&st->max_rel_dev_bits, 0ull);
+        volatile DetectStats* h = host_out;
+        h->flagged = fl;
+        h->max_rel_dev_bits = mb;
+        __threadfence_system();
+        *ticket = 0u;
+      }
+    }
+  }
+}
+
+inline int pick_positions(int work_per_position) {
+  // slices S ~ work/4 (a few serial steps per thread), P = 256 / S positions per block
+  int S = 16;
+  while (S < 256 && S * 4 < work_per_position) S <<= 1;
+  return 256 / S;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -591,20 +714,13 @@ int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N
 
 int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
                       int pad, int E, cudaStream_t s) {
-  static bool carve = false;
-  if (!carve && getenv("FTC_CARVEOUT")) {
-    cudaFuncSetAttribute(k_co5_sliced<3>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_co5_sliced<5>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_co5_sliced<0>, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
-  const int g = (E * E + 31) / 32, t = 32 * kDetSlices;
+  const int P = pick_positions(C);
+  const int g = (E * E + P - 1) / P;
   switch (R) {
-    case 1: FTC_LAUNCH(k_co5_sliced<1><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
-    case 3: FTC_LAUNCH(k_co5_sliced<3><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
-    case 5: FTC_LAUNCH(k_co5_sliced<5><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
-    case 7: FTC_LAUNCH(k_co5_sliced<7><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
-    default: FTC_LAUNCH(k_co5_sliced<0><<<g, t, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E)); break;
+    case 1: FTC_LAUNCH(k_co5_adapt<1><<<g, 256, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E, P)); break;
+    case 3: FTC_LAUNCH(k_co5_adapt<3><<<g, 256, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E, P)); break;
+    case 5: FTC_LAUNCH(k_co5_adapt<5><<<g, 256, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E, P)); break;
+    default: FTC_LAUNCH(k_co5_adapt<0><<<g, 256, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E, P)); break;
   }
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
@@ -613,14 +729,9 @@ int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, 
 int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                       const double* agg, double tau, DetectStats* st, unsigned int* ticket,
                       DetectStats* host_out, cudaStream_t s) {
-  static bool carve = false;
-  if (!carve && getenv("FTC_CARVEOUT")) {  // experiment: keep the conv's L1/SMEM split
-    cudaFuncSetAttribute(k_detect_so5, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    carve = true;
-  }
-  FTC_LAUNCH(k_detect_so5<<<(E2 + 31) / 32, 32 * kDetSlices, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg,
-                                                                      tau, st, ticket, host_out));
+  const int P = pick_positions(N * parts);
+  FTC_LAUNCH(k_detect_adapt<<<(E2 + P - 1) / P, 256, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st, ticket,
+                                                             host_out, P));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -21,27 +21,81 @@ __device__ __forceinline__ float act_fn(float v, int act) {
 }
 
 // out[n,c,ox,oy] = max over the k x k window (stride s, padding p, -inf padding)
-// of act(in[n,c,.,.]); k = 1, s = 1 is a plain activation.
-__global__ void k_act_pool(const float* __restrict__ in, float* __restrict__ out, int NC, int H,
-                           int act, int k, int s, int p, int Ho) {
-  const long long total = (long long)NC * Ho * Ho;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int oy = (int)(e % Ho), ox = (int)((e / Ho) % Ho);
-    const long long nc = e / ((long long)Ho * Ho);
-    const float* src = in + nc * H * H;
-    float m = -INFINITY;
-    for (int i = 0; i < k; ++i) {
-      const int x = ox * s - p + i;
-      if (x < 0 || x >= H) continue;
-      for (int j = 0; j < k; ++j) {
-        const int y = oy * s - p + j;
-        if (y < 0 || y >= H) continue;
-        m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
+// of act(in[n,c,.,.]); k = 1, s = 1 is a plain activation.  Grid: y = (n, c) plane
+// (strided when N*C exceeds the grid limit), x = output positions of the plane; 32-bit
+// index math (a 64-bit div/mod per element made this kernel integer-bound).
+template <int KT>
+__global__ void __launch_bounds__(256) k_act_pool(const float* __restrict__ in, float* __restrict__ out,
+                                                 int NC, int H, int act, int kr, int s, int p, int Ho) {
+  constexpr int kPlanes = 4;  // planes per thread: their window loads are all in flight
+  const int k = KT > 0 ? KT : kr;
+  const int plane = Ho * Ho;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= plane) return;
+  const int ox = idx / Ho, oy = idx - (idx / Ho) * Ho;
+  const int x0 = ox * s - p, y0 = oy * s - p;
+  for (int nc0 = blockIdx.y * kPlanes; nc0 < NC; nc0 += gridDim.y * kPlanes) {
+    if constexpr (KT > 0) {
+      float v[kPlanes][KT * KT];
+#pragma unroll
+      for (int u = 0; u < kPlanes; ++u) {
+        const float* src = in + (long long)(nc0 + u) * H * H;
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const int x = x0 + i, y = y0 + j;
+            const bool ok = nc0 + u < NC && x >= 0 && x < H && y >= 0 && y < H;
+            v[u][i * KT + j] = ok ? __ldg(src + x * H + y) : -INFINITY;
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < kPlanes; ++u) {
+        if (nc0 + u >= NC) break;
+        float m = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const int x = x0 + i, y = y0 + j;
+            // padding positions are skipped (not act(-inf)) exactly as the generic path
+            if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[u][i * KT + j], act));
+          }
+        out[(long long)(nc0 + u) * plane + idx] = m;
+      }
+    } else {
+      for (int u = 0; u < kPlanes && nc0 + u < NC; ++u) {
+        const float* src = in + (long long)(nc0 + u) * H * H;
+        float m = -INFINITY;
+        for (int i = 0; i < k; ++i) {
+          const int x = x0 + i;
+          if (x < 0 || x >= H) continue;
+          for (int j = 0; j < k; ++j) {
+            const int y = y0 + j;
+            if (y < 0 || y >= H) continue;
+            m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
+          }
+        }
+        out[(long long)(nc0 + u) * plane + idx] = m;
       }
     }
-    out[e] = m;
   }
+}
+
+int launch_act_pool(const float* in, float* out, int NC, int H, int act, int k, int s, int p, int Ho,
+                    cudaStream_t st) {
+  const int gy = (NC + 3) / 4;
+  const dim3 g((unsigned)((Ho * Ho + 255) / 256), (unsigned)(gy < 65535 ? gy : 65535));
+  if (k == 3)
+    FTC_LAUNCH(k_act_pool<3><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
+  else if (k == 2)
+    FTC_LAUNCH(k_act_pool<2><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
+  else if (k == 1)
+    FTC_LAUNCH(k_act_pool<1><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
+  else
+    FTC_LAUNCH(k_act_pool<0><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
 }
 
 __global__ void k_add_act(const float* __restrict__ a, const float* __restrict__ b,
@@ -53,15 +107,14 @@ __global__ void k_add_act(const float* __restrict__ a, const float* __restrict__
 
 // out (N,C,Ho,Ho) = in shifted by (-lo) with zero fill: Ho = H + lo + hi; negative
 // hi crops the bottom/right edge.
-__global__ void k_pad_crop(const float* __restrict__ in, float* __restrict__ out, int NC, int H,
-                           int lo, int Ho) {
-  const long long total = (long long)NC * Ho * Ho;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int y = (int)(e % Ho) - lo, x = (int)((e / Ho) % Ho) - lo;
-    const long long nc = e / ((long long)Ho * Ho);
-    out[e] = (x >= 0 && x < H && y >= 0 && y < H) ? in[(nc * H + x) * H + y] : 0.f;
-  }
+__global__ void __launch_bounds__(256) k_pad_crop(const float* __restrict__ in, float* __restrict__ out, int NC,
+                                                 int H, int lo, int Ho) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Ho * Ho) return;
+  const int x = idx / Ho - lo, y = idx - (idx / Ho) * Ho - lo;
+  const bool ok = x >= 0 && x < H && y >= 0 && y < H;
+  for (int nc = blockIdx.y; nc < NC; nc += gridDim.y)
+    out[(long long)nc * Ho * Ho + idx] = ok ? __ldg(in + ((long long)nc * H + x) * H + y) : 0.f;
 }
 
 inline int grid_for(long long n) {
@@ -86,10 +139,7 @@ int ftc_glue_act_pool(const float* in, float* out, int32_t N, int32_t C, int32_t
   const int Ho = (H + 2 * p - k) / s + 1;
   if (Ho_out) *Ho_out = Ho;
   if (!in || !out) return FTC_OK;  // shape query
-  FTC_LAUNCH(k_act_pool<<<grid_for((long long)N * C * Ho * Ho), 256, 0, (cudaStream_t)stream>>>(
-      in, out, N * C, H, act, k, s, p, Ho));
-  FTC_CUDA_CHECK(cudaGetLastError());
-  return FTC_OK;
+  return launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, (cudaStream_t)stream);
 }
 
 int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t act,
@@ -104,9 +154,10 @@ int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int3
   // the AlexNet step.)
   const int Ho = (H + 2 * p - k) / s + 1;
   const long long per = (long long)C * Ho * Ho;
-  FTC_LAUNCH(k_act_pool<<<grid_for((long long)N * per), 256, 0, (cudaStream_t)stream>>>(
-      in, out, N * C, H, act, k, s, p, Ho));
-  FTC_CUDA_CHECK(cudaGetLastError());
+  {
+    const int st = launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, (cudaStream_t)stream);
+    if (st != FTC_OK) return st;
+  }
   return launch_input_checksums(out, N, per, cd1, cd2, (cudaStream_t)stream);
 }
 
@@ -123,8 +174,8 @@ int ftc_glue_pad_crop(const float* in, float* out, int32_t N, int32_t C, int32_t
     set_error(FTC_CONFIG_ERROR, "bad pad/crop");
     return FTC_CONFIG_ERROR;
   }
-  FTC_LAUNCH(k_pad_crop<<<grid_for((long long)N * C * Ho * Ho), 256, 0, (cudaStream_t)stream>>>(
-      in, out, N * C, H, lo, Ho));
+  const dim3 g((unsigned)((Ho * Ho + 255) / 256), (unsigned)(N * C < 65535 ? N * C : 65535));
+  FTC_LAUNCH(k_pad_crop<<<g, 256, 0, (cudaStream_t)stream>>>(in, out, N * C, H, lo, Ho));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
