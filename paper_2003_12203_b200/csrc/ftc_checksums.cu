@@ -144,27 +144,6 @@ __global__ void k_conv_f64_exact(const TI* __restrict__ in, const TW* __restrict
   out[idx] = acc;
 }
 
-// Co5 = conv_block(Cd1, Cw1) for the clean path: one warp per output position,
-// lanes stride over K, fixed xor-shuffle tree (deterministic run to run).
-__global__ void k_co5_fast(const double* __restrict__ cd1, const double* __restrict__ cw1,
-                           double* __restrict__ co5, int C, int H, int R, int U, int pad, int E) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= E * E) return;
-  const int x = warp / E, y = warp % E;
-  const int RR = R * R, K = C * RR;
-  double acc = 0.0;
-  for (int k = lane; k < K; k += 32) {
-    const int c = k / RR, t = k % RR, i = t / R, j = t % R;
-    const int hh = U * x + i - pad, ww = U * y + j - pad;
-    if (hh >= 0 && hh < H && ww >= 0 && ww < H)
-      acc = fma(cd1[((long long)c * H + hh) * H + ww], cw1[k], acc);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) co5[warp] = acc;
-}
-
 // BiasAdjuster ctor (checksums.hpp:199-208) at T=double
 __global__ void k_bias_aggregates(const float* __restrict__ b, int M, double* agg) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -265,20 +244,6 @@ __device__ __forceinline__ void detect_one(double c, double s, double tau, int* 
   if (*bad) atomicAdd(flagged, 1);
 }
 
-__global__ void k_detect_fast(const double* __restrict__ co5, const double* __restrict__ rowsum,
-                              int parts, int N, int E2, int bias, const double* agg, double tau,
-                              DetectStats* st) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= E2) return;
-  double s = 0.0;
-  const long long slab = (long long)N * E2;
-  for (int n = 0; n < N; ++n)
-    for (int q = 0; q < parts; ++q) s += rowsum[q * slab + (long long)n * E2 + f];
-  if (bias) s -= (double)N * agg[0];
-  bool bad;
-  detect_one(co5[f], s, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
-}
-
 __global__ void k_detect_exact(const double* __restrict__ co5, const double* __restrict__ so5,
                                int E2, double tau, uint8_t* mask, DetectStats* st) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -330,160 +295,6 @@ __global__ void __launch_bounds__(128) k_cd1_fast(const float* __restrict__ D, i
   double2* o = reinterpret_cast<double2*>(cd1) + 2 * e;
   o[0] = make_double2(a0, a1);
   o[1] = make_double2(a2, a3);
-}
-
-// Clean-path CoC-D: one warp per position f; lanes stride over the (row-sum slab,
-// image) pairs of the fused epilogue sums, fixed xor-shuffle tree (deterministic).
-__global__ void k_detect_warp(const double* __restrict__ co5, const double* __restrict__ rowsum,
-                              int parts, int N, int E2, int bias, const double* agg, double tau,
-                              DetectStats* st) {
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (f >= E2) return;
-  const long long slab = (long long)N * E2;
-  const int terms = N * parts;
-  double s = 0.0;
-  for (int t = lane; t < terms; t += 32) {
-    const int q = t / N, n = t - q * N;
-    s += rowsum[q * slab + (long long)n * E2 + f];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    if (bias) s -= (double)N * agg[0];
-    bool bad;
-    detect_one(co5[f], s, tau, &st->flagged, &st->max_rel_dev_bits, &bad);
-  }
-}
-
-// Clean-path Co5 = conv_block(Cd1, Cw1) (checksums.hpp:157): a block owns 32
-// consecutive positions (lanes, coalesced Cd1 loads) x 16 channel slices (warps),
-// combined in a fixed order.  Runs on the side stream, concurrently with the conv.
-constexpr int kDetSlices = 16;
-template <int RT>  // RT > 0: compile-time kernel side (taps unrolled, loads issued first)
-__global__ void __launch_bounds__(32 * kDetSlices) k_co5_sliced(
-    const double* __restrict__ cd1, const double* __restrict__ cw1, double* __restrict__ co5, int C,
-    int H, int Rrt, int U, int pad, int E) {
-  __shared__ double red[kDetSlices][32];
-  const int R = RT > 0 ? RT : Rrt;
-  const int E2 = E * E;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  double c5 = 0.0;
-  if (f < E2) {
-    const int x = f / E, y = f - (f / E) * E;
-    const int hb = x * U - pad, wb = y * U - pad;
-    const int RR = R * R;
-    if constexpr (RT > 0) {
-      bool rok[RT], cok[RT];
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        rok[i] = (unsigned)(hb + i) < (unsigned)H;
-        cok[i] = (unsigned)(wb + i) < (unsigned)H;
-      }
-      for (int c = w; c < C; c += kDetSlices) {
-        const double* src = cd1 + (long long)c * H * H + (long long)hb * H + wb;
-        const double* ker = cw1 + c * RR;
-        double v[RT * RT];
-#pragma unroll
-        for (int i = 0; i < RT; ++i)
-#pragma unroll
-          for (int j = 0; j < RT; ++j) v[i * RT + j] = (rok[i] && cok[j]) ? __ldg(src + i * H + j) : 0.0;
-#pragma unroll
-        for (int t = 0; t < RT * RT; ++t) c5 = fma(v[t], __ldg(ker + t), c5);
-      }
-    } else {
-      for (int c = w; c < C; c += kDetSlices) {
-        const double* src = cd1 + (long long)c * H * H;
-        const double* ker = cw1 + c * RR;
-        for (int i = 0; i < R; ++i) {
-          const int hh = hb + i;
-          if (hh < 0 || hh >= H) continue;
-          for (int j = 0; j < R; ++j) {
-            const int ww = wb + j;
-            if (ww < 0 || ww >= H) continue;
-            c5 = fma(src[hh * H + ww], ker[i * R + j], c5);
-          }
-        }
-      }
-    }
-  }
-  red[w][lane] = c5;
-  __syncthreads();
-  if (w == 0 && f < E2) {
-    double cc = 0.0;
-#pragma unroll
-    for (int q = 0; q < kDetSlices; ++q) cc += red[q][lane];
-    co5[f] = cc;
-  }
-}
-
-// Clean-path CoC-D after the conv: So5[f] = sum of the fused epilogue row sums over
-// (slab, image) (16 slices per 32 positions, fixed-order combine), compared with the
-// precomputed Co5 (values_differ).  The last block to finish publishes {flagged,
-// max_rel_dev} into the mapped host record and re-zeroes the device counters for
-// the next call (no memset / copy nodes on the clean path).
-__global__ void __launch_bounds__(32 * kDetSlices) k_detect_so5(
-    const double* __restrict__ co5, const double* __restrict__ rowsum, int parts, int N, int E2,
-    int bias, const double* agg, double tau, DetectStats* st, unsigned int* ticket,
-    DetectStats* host_out) {
-  __shared__ double red[kDetSlices][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  double s5 = 0.0;
-  if (f < E2) {
-    const long long slab = (long long)N * E2;
-    const int terms = N * parts;
-    for (int t = w; t < terms; t += kDetSlices) {
-      const int q = t / N, n = t - q * N;
-      s5 += rowsum[q * slab + (long long)n * E2 + f];
-    }
-  }
-  red[w][lane] = s5;
-  __syncthreads();
-  if (w == 0) {
-    int bad = 0;
-    unsigned long long devb = 0ull;
-    if (f < E2) {
-      double ss = 0.0;
-#pragma unroll
-      for (int q = 0; q < kDetSlices; ++q) ss += red[q][lane];
-      if (bias) ss -= (double)N * agg[0];
-      const double c = co5[f];
-      double den = fabs(c);
-      if (den < fabs(ss)) den = fabs(ss);
-      if (den < 1.0) den = 1.0;
-      const double dev = fabs(c - ss) / den;
-      if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
-      bad = values_differ(c, ss, tau) ? 1 : 0;
-    }
-    // one atomic per block (non-negative doubles order as u64; NaN devs excluded)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      bad += __shfl_xor_sync(0xffffffffu, bad, o);
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
-      devb = other > devb ? other : devb;
-    }
-    if (lane == 0) {
-      if (bad) atomicAdd(&st->flagged, bad);
-      if (devb) atomicMax(&st->max_rel_dev_bits, devb);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned int done = atomicAdd(ticket, 1u);
-    if (done == gridDim.x - 1) {  // last block: publish and reset
-      __threadfence();
-      const int fl = atomicExch(&st->flagged, 0);
-      const unsigned long long mb = atomicExch(&st->max_rel_dev_bits, 0ull);
-      volatile DetectStats* h = host_out;
-      h->flagged = fl;
-      h->max_rel_dev_bits = mb;
-      __threadfence_system();
-      *ticket = 0u;
-    }
-  }
 }
 
 // Adaptive forms for the clean path: a 256-thread block covers P positions x S slices
@@ -655,14 +466,6 @@ int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64
   return FTC_OK;
 }
 
-int launch_co5_fast(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
-                    int pad, int E, cudaStream_t s) {
-  const long long threads = (long long)E * E * 32;
-  FTC_LAUNCH(k_co5_fast<<<blocks_for(threads), kThreads, 0, s>>>(cd1, cw1, co5, C, H, R, U, pad, E));
-  FTC_CUDA_CHECK(cudaGetLastError());
-  return FTC_OK;
-}
-
 int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s) {
   FTC_LAUNCH(k_bias_aggregates<<<1, 32, 0, s>>>(bias, M, agg));
   FTC_CUDA_CHECK(cudaGetLastError());
@@ -687,27 +490,12 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
   return FTC_OK;
 }
 
-int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
-                       const double* agg, double tau, DetectStats* st, cudaStream_t s) {
-  FTC_LAUNCH(k_detect_fast<<<blocks_for(E2), kThreads, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st));
-  FTC_CUDA_CHECK(cudaGetLastError());
-  return FTC_OK;
-}
-
 int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s) {
   if (per % 4 != 0 || ((uintptr_t)D % 16) != 0 || ((uintptr_t)cd1 % 16) != 0) {
     // plane size not a multiple of 4: the exact kernel produces Cd1 (and Cd2)
     return FTC_CONFIG_ERROR;
   }
   FTC_LAUNCH(k_cd1_fast<<<blocks_for(per / 4, 128), 128, 0, s>>>(D, N, per / 4, cd1));
-  FTC_CUDA_CHECK(cudaGetLastError());
-  return FTC_OK;
-}
-
-int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
-                       const double* agg, double tau, DetectStats* st, cudaStream_t s) {
-  FTC_LAUNCH(k_detect_warp<<<blocks_for((long long)E2 * 32), kThreads, 0, s>>>(co5, rowsum, parts, N, E2,
-                                                                              bias, agg, tau, st));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -154,9 +154,6 @@ int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, d
 int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64, double* out,
                           int B, int Cin, int H, int Mo, int Ckw, int R, int U, int pad,
                           int groups, int E, cudaStream_t s);
-// Co5 for the clean path: warp-split K, fixed shuffle order (deterministic)
-int launch_co5_fast(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
-                    int pad, int E, cudaStream_t s);
 // bias aggregates: agg[0]=sum_b, agg[1]=sum_mb (BiasAdjuster ctor, checksums.hpp:199-208)
 int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s);
 
@@ -169,18 +166,12 @@ struct VirtualO {  // FP32 O plus FP64 overrides left by the verifier's rollback
 int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t which,
                              const float* bias, const double* agg, double* const so[7],
                              cudaStream_t s);
-// clean-path CoC-D: so5 = sum_n rowsum (bias adjusted) vs co5; stats into dev[0..]
-int launch_detect_fast(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
-                       const double* agg, double tau, DetectStats* st, cudaStream_t s);
 // clean path: Cd1 only, parallel over positions (FTC_CONFIG_ERROR when the plane size
 // is odd -> caller uses the exact kernel)
 int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s);
-int launch_detect_warp(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
-                       const double* agg, double tau, DetectStats* st, cudaStream_t s);
-// clean path CoC-D with Co5 computed in the same kernel
-// clean path: Co5 on the side stream, then So5 from the fused row sums + compare;
-// the last block publishes the record into mapped host memory (host_out) and
-// re-zeroes st/ticket for the next call
+// clean path: Co5 (adaptive positions x channel slices), then So5 from the fused row
+// sums + compare; the last block publishes the record into mapped host memory
+// (host_out) and re-zeroes st/ticket for the next call
 int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
                       int pad, int E, cudaStream_t s);
 int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
