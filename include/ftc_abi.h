@@ -190,6 +190,15 @@ int ftc_protected_conv_launch_ck(ftc_layer* layer, const ftc_plan* plan, const f
                                  const double* cd1, const double* cd2, const ftc_fault* faults,
                                  int32_t n_faults, void* stream);
 
+/* Channel-last input staging for the TMA im2col engine (C % 32 == 0 layers): the layer
+ * keeps an NHWC copy of its input that every launch refreshes from D.  A producer that
+ * already wrote D in NHWC form into that buffer (ftc_glue_act_pool_nhwc) calls
+ * _input_nhwc_ready so the next launch (protected or not) skips the refresh; D itself
+ * must still hold the same values in NCHW (checksums, error path).  *nhwc = NULL when
+ * the layer's engine does not stage its input. */
+int ftc_layer_input_nhwc(ftc_layer* layer, float** nhwc);
+int ftc_layer_input_nhwc_ready(ftc_layer* layer, const float* D);
+
 /* Instrumentation for bench.py: when enabled, CUDA events bracket the conv kernel
  * of every protected/unprotected call on its launching stream; _kernel_time
  * returns the accumulated device time (ms) and launch count (reset if `reset`).
@@ -239,6 +248,12 @@ int ftc_glue_act_pool(const float* in, float* out, int32_t N, int32_t C, int32_t
  * input_checksums of `out` exactly, checksums.hpp:100-107). */
 int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int32_t H, int32_t act,
                          int32_t k, int32_t s, int32_t p, double* cd1, double* cd2, void* stream);
+/* ftc_glue_act_pool(_ck) that also writes its output channel-last into out_nhwc
+ * (N, Ho*Ho, C) for the next layer's TMA im2col staging (C % 32 == 0); cd1/cd2 may
+ * be NULL (no checksums). */
+int ftc_glue_act_pool_nhwc(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
+                           int32_t act, int32_t k, int32_t s, int32_t p, double* cd1, double* cd2,
+                           void* stream);
 /* out = act(a + b) elementwise over n values (b may be NULL) */
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act,
                      void* stream);

@@ -24,6 +24,7 @@ EXPORTS = (
     "ftc_verify_kernel", "ftc_layer_set_timing", "ftc_layer_kernel_time", "ftc_kernel_launches",
     "ftc_glue_act_pool", "ftc_glue_add_act", "ftc_glue_pad_crop", "ftc_protected_conv_launch_ck",
     "ftc_glue_act_pool_ck", "ftc_conv_forward_host", "ftc_protected_check",
+    "ftc_layer_input_nhwc", "ftc_layer_input_nhwc_ready", "ftc_glue_act_pool_nhwc",
 )
 
 
@@ -94,6 +95,9 @@ def lib():
         L.ftc_protected_conv_launch_ck.argtypes = [vp, C.POINTER(Plan), vp, vp, vp, vp, C.POINTER(Fault),
                                                    i32, vp]
         L.ftc_glue_act_pool_ck.argtypes = [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
+        L.ftc_glue_act_pool_nhwc.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
+        L.ftc_layer_input_nhwc.argtypes = [vp, C.POINTER(vp)]
+        L.ftc_layer_input_nhwc_ready.argtypes = [vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         _lib = L

@@ -82,6 +82,61 @@ __global__ void __launch_bounds__(256) k_act_pool(const float* __restrict__ in, 
   }
 }
 
+// act + pool of one image's 32-channel x 8-position tile, written NCHW and, through
+// shared memory, NHWC (the next conv's TMA im2col input): loads by channel rows of 8
+// consecutive positions, stores by position rows of 32 channels (128 bytes)
+template <int KT>
+__global__ void __launch_bounds__(256) k_act_pool_t(const float* __restrict__ in, float* __restrict__ out,
+                                                   float* __restrict__ out_t, int C, int H, int act, int kr, int s,
+                                                   int p, int Ho) {
+  __shared__ float tile[8][33];
+  const int k = KT > 0 ? KT : kr;
+  const int plane = Ho * Ho;
+  const int tid = threadIdx.x;
+  const int cl = tid >> 3, pl = tid & 7;
+  const int c = blockIdx.y * 32 + cl, pos = blockIdx.x * 8 + pl;
+  const long long n = blockIdx.z;
+  float m = -INFINITY;
+  if (pos < plane) {
+    const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
+    const int x0 = ox * s - p, y0 = oy * s - p;
+    const float* src = in + (n * C + c) * H * H;
+    if constexpr (KT > 0) {
+      float v[KT * KT];
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          const int x = x0 + i, y = y0 + j;
+          v[i * KT + j] = (x >= 0 && x < H && y >= 0 && y < H) ? __ldg(src + x * H + y) : 0.f;
+        }
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          const int x = x0 + i, y = y0 + j;
+          if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[i * KT + j], act));
+        }
+    } else {
+      for (int i = 0; i < k; ++i) {
+        const int x = x0 + i;
+        if (x < 0 || x >= H) continue;
+        for (int j = 0; j < k; ++j) {
+          const int y = y0 + j;
+          if (y < 0 || y >= H) continue;
+          m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
+        }
+      }
+    }
+    out[(n * C + c) * plane + pos] = m;
+  }
+  tile[pl][cl] = m;
+  __syncthreads();
+  const int wc = tid & 31, wp = tid >> 5;
+  const int spos = blockIdx.x * 8 + wp;
+  if (spos < plane) out_t[(n * plane + spos) * C + blockIdx.y * 32 + wc] = tile[wp][wc];
+}
+
 int launch_act_pool(const float* in, float* out, int NC, int H, int act, int k, int s, int p, int Ho,
                     cudaStream_t st) {
   const int gy = (NC + 3) / 4;
@@ -159,6 +214,29 @@ int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int3
     if (st != FTC_OK) return st;
   }
   return launch_input_checksums(out, N, per, cd1, cd2, (cudaStream_t)stream);
+}
+
+int ftc_glue_act_pool_nhwc(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
+                           int32_t act, int32_t k, int32_t s, int32_t p, double* cd1, double* cd2,
+                           void* stream) {
+  if (k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || !in || !out || !out_nhwc || C % 32 || (!cd1) != (!cd2)) {
+    set_error(FTC_CONFIG_ERROR, "bad pooling window, null buffer or C % 32 != 0");
+    return FTC_CONFIG_ERROR;
+  }
+  const int Ho = (H + 2 * p - k) / s + 1;
+  const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)N);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 3)
+    FTC_LAUNCH(k_act_pool_t<3><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
+  else if (k == 2)
+    FTC_LAUNCH(k_act_pool_t<2><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
+  else if (k == 1)
+    FTC_LAUNCH(k_act_pool_t<1><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
+  else
+    FTC_LAUNCH(k_act_pool_t<0><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  if (!cd1) return FTC_OK;
+  return launch_input_checksums(out, N, (long long)C * Ho * Ho, cd1, cd2, st);
 }
 
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act, void* stream) {

@@ -64,6 +64,8 @@ struct ftc_layer {
   double *cd1 = nullptr, *cd2 = nullptr;
   double* co5f = nullptr;
   double* so5acc = nullptr;  // fused clean path: So5 accumulator (zero between calls)
+  bool nhwc_ready = false;   // the next conv's NHWC input copy is already staged (one-shot)
+  const float* D_staged = nullptr;  // the D it was staged from (set by the caller's next launch)
   double *rowsum = nullptr, *rowsum_m = nullptr;
   DetectStats* stats = nullptr;
   DetectStats* stats_h = nullptr;  // pinned
@@ -170,8 +172,12 @@ int run_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults
   // fault injection) runs through the SIMT engine.
   if (use_tc(L) && W == L->W) {
     if (sums) L->rs_parts = tc_rowsum_parts(L->tc);
+    // a producer staged the NHWC copy of exactly this D (whole batch only)
+    if (L->nhwc_ready && D == L->D_staged && img_lo == 0 && img_hi == L->d.N) a.dt_ready = true;
+    L->nhwc_ready = false;
     return conv_tc_launch(L->tc, a, s);
   }
+  L->nhwc_ready = false;
   if (sums) L->rs_parts = 1;
   return conv_simt_launch(a, s);
 }
@@ -797,6 +803,20 @@ int ftc_conv_forward_host(ftc_layer* L, const float* D_host, float* O_host, void
   CK(ftc_conv_forward(L, L->D_host_buf, L->O_host_buf, stream));
   FTC_CUDA_CHECK(cudaMemcpyAsync(O_host, L->O_host_buf, L->nO * sizeof(float), cudaMemcpyDeviceToHost, s));
   FTC_CUDA_CHECK(cudaStreamSynchronize(s));
+  return FTC_OK;
+}
+
+int ftc_layer_input_nhwc(ftc_layer* L, float** nhwc) {
+  if (!L || !nhwc) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  *nhwc = (use_tc(L) && tc_im2col(L->tc)) ? tc_nhwc_buffer(L->tc) : nullptr;
+  return FTC_OK;
+}
+
+int ftc_layer_input_nhwc_ready(ftc_layer* L, const float* D) {
+  if (!L || !D) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (!(use_tc(L) && tc_im2col(L->tc))) RET_ERR(FTC_INVALID_ARGUMENT, "layer does not stage an NHWC input");
+  L->nhwc_ready = true;
+  L->D_staged = D;
   return FTC_OK;
 }
 

@@ -232,6 +232,16 @@ class ProtectedConv:
         torch = _torch()
         return torch.empty(self.out_shape, dtype=torch.float32, device=D.device)
 
+    def input_nhwc(self):
+        """Device pointer of the layer's NHWC input staging buffer (TMA im2col engine) or None."""
+        p = C.c_void_p()
+        _check(_abi.lib().ftc_layer_input_nhwc(self.h, C.byref(p)), "input_nhwc")
+        return p.value
+
+    def input_nhwc_ready(self, D):
+        """Declare that the staging buffer already holds D (NHWC) for the next launch on D."""
+        _check(_abi.lib().ftc_layer_input_nhwc_ready(self.h, _ptr(D)), "input_nhwc_ready")
+
     def conv_forward(self, D, O=None, stream=None):
         """conv_forward(D, W, bias, p) on device (conv.hpp:114-131)."""
         O = self._empty_out(D) if O is None else O

@@ -231,6 +231,19 @@ class ProtectedNet:
                 c, h = self.sh[op.dst]
                 self.ck[op.dst] = (torch.empty((c, h, h), dtype=torch.float64, device=dev),
                                    torch.empty((c, h, h), dtype=torch.float64, device=dev))
+        # an act+pool whose output feeds exactly one conv staged channel-last (TMA im2col)
+        # writes that layer's NHWC copy in the same pass
+        consumers = {}
+        for op in net["ops"]:
+            if isinstance(op, Conv):
+                consumers.setdefault(op.src, []).append(op.dst)
+        self.nhwc_target = {}
+        for op in net["ops"]:
+            if isinstance(op, ActPool) and len(consumers.get(op.dst, [])) == 1:
+                L = self.layers[consumers[op.dst][0]]
+                ptr = L.input_nhwc()
+                if ptr:
+                    self.nhwc_target[op.dst] = (L, ptr)
         self.out_name = net.get("output", "out")
         self.flops = sum(2.0 * batch * op.M * E * E * Cin * op.R * op.R for op, Cin, H, E in self.convs)
 
@@ -242,7 +255,16 @@ class ProtectedNet:
         s = stream.cuda_stream
         if isinstance(op, ActPool):
             c, h = self.sh[op.src]
-            if op.dst in self.ck:
+            if op.dst in self.nhwc_target:
+                Lc, ptr = self.nhwc_target[op.dst]
+                cd1, cd2 = self.ck.get(op.dst, (None, None))
+                _check(L.ftc_glue_act_pool_nhwc(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), ptr,
+                                                self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
+                                                cd1.data_ptr() if cd1 is not None else None,
+                                                cd2.data_ptr() if cd2 is not None else None, s),
+                       "act_pool_nhwc")
+                Lc.input_nhwc_ready(self.buf[op.dst])
+            elif op.dst in self.ck:
                 cd1, cd2 = self.ck[op.dst]
                 _check(L.ftc_glue_act_pool_ck(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(),
                                               self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
