@@ -1,0 +1,119 @@
+"""GPU tests of the engine paths added for speed: TMA im2col geometry, the act+pool glue
+that stages the next layer's NHWC copy, the staging guard, and the opt-in fused
+clean-path CoC-D (verdict parity with run_protected_layer<double>)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+from conftest import ROOT
+
+
+def _rel(a, b):
+    return np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,C,H,M,R,s,p", [(2, 32, 15, 40, 3, 2, 1), (3, 64, 9, 24, 1, 1, 0), (2, 32, 11, 70, 5, 1, 2),
+                                           (2, 96, 13, 130, 3, 1, 1), (1, 32, 17, 32, 3, 2, 0)])
+def test_tma_im2col_conv_geometry(N, C, H, M, R, s, p):
+    """C % 32 == 0 layers run the TMA im2col engine: strides, paddings, 1x1/3x3/5x5 taps,
+    partial pixel tiles and partial N tiles against conv_forward<float>."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import synth
+    D = synth.relu_like((N, C, H, H), 5)
+    W = synth.he_normal(M, C, R, 6)
+    B = synth.uniform((M,), -0.1, 0.1, 7)
+    L = F.ProtectedConv(W, B, F.ConvParams(stride=s, pad=p, bias_enabled=True), N, H)
+    Og = L.conv_forward(torch.from_numpy(D).cuda()).cpu().numpy()
+    Or = O.conv_f32(O.dims(N, C, H, M, R, s, p, 1, True), D, W, B)
+    assert _rel(Og, Or).max() <= 1e-5
+    L.close()
+
+
+@pytest.mark.gpu
+def test_act_pool_nhwc_glue_bitwise():
+    """ftc_glue_act_pool_nhwc == ftc_glue_act_pool_ck (NCHW output and exact Cd1/Cd2)
+    bitwise, and its NHWC output is exactly the channel-last transpose."""
+    import torch
+    from paper_2003_12203_b200 import _abi
+    L = _abi.lib()
+    rng = np.random.default_rng(3)
+    N, C, H, k, s, p = 3, 64, 27, 3, 2, 0
+    Ho = (H + 2 * p - k) // s + 1
+    x = torch.from_numpy(rng.standard_normal((N, C, H, H)).astype(np.float32)).cuda()
+    out_a = torch.empty((N, C, Ho, Ho), device="cuda")
+    out_b = torch.empty_like(out_a)
+    nhwc = torch.empty((N, Ho, Ho, C), device="cuda")
+    cd = [torch.empty((C, Ho, Ho), dtype=torch.float64, device="cuda") for _ in range(4)]
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.ftc_glue_act_pool_ck(x.data_ptr(), out_a.data_ptr(), N, C, H, 1, k, s, p, cd[0].data_ptr(),
+                                  cd[1].data_ptr(), st) == 0
+    assert L.ftc_glue_act_pool_nhwc(x.data_ptr(), out_b.data_ptr(), nhwc.data_ptr(), N, C, H, 1, k, s, p,
+                                    cd[2].data_ptr(), cd[3].data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out_a, out_b)
+    assert torch.equal(nhwc, out_b.permute(0, 2, 3, 1))
+    assert torch.equal(cd[0], cd[2]) and torch.equal(cd[1], cd[3])
+
+
+@pytest.mark.gpu
+def test_nhwc_staging_guard():
+    """A staging declared for one D is ignored when the layer is launched on another D."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import synth
+    N, C, H, M, R = 2, 32, 12, 48, 3
+    W = synth.he_normal(M, C, R, 1)
+    L = F.ProtectedConv(W, None, F.ConvParams(pad=1), N, H)
+    assert L.input_nhwc() is not None
+    D1 = torch.from_numpy(synth.relu_like((N, C, H, H), 1)).cuda()
+    D2 = torch.from_numpy(synth.relu_like((N, C, H, H), 2)).cuda()
+    # declare a staging for D1 (the buffer holds whatever it holds), then run on D2: the
+    # launch must restage from D2 rather than trust the declaration
+    L.input_nhwc_ready(D1)
+    O2 = L.conv_forward(D2).cpu().numpy()
+    Or = O.conv_f32(O.dims(N, C, H, M, R, 1, 1, 1, False), D2.cpu().numpy(), W, None)
+    assert _rel(O2, Or).max() <= 1e-5
+    L.close()
+
+
+_FUSED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {oracle!r})
+import paper_2003_12203_b200 as F
+from paper_2003_12203_b200 import synth
+import oracle_py as O
+N, C, H, M, R = 4, 32, 12, 48, 3
+D = synth.relu_like((N, C, H, H), 11); W = synth.he_normal(M, C, R, 12); B = synth.uniform((M,), -0.1, 0.1, 13)
+L = F.ProtectedConv(W, B, F.ConvParams(pad=1, bias_enabled=True), N, H)
+Dg = torch.from_numpy(D).cuda()
+plan = F.LayerPlan(rc_enabled=True, clc_enabled=True, tau=1e-3)
+O0, rep = L.protected(Dg, plan)
+assert not rep.detected
+O0 = O0.cpu().numpy()
+dims = O.dims(N, C, H, M, R, 1, 1, 1, True)
+rng = np.random.default_rng(5)
+for t in range(12):
+    n, m, x, y = int(rng.integers(N)), int(rng.integers(M)), int(rng.integers(H)), int(rng.integers(H))
+    bit = int(rng.integers(20, 31))
+    _, r = L.protected(Dg, plan, [F.output_bitflip(n, m, x, y, bit)])
+    Os = O0.copy(); Os[n, m, x, y] = synth.flip32(Os[n, m, x, y], bit)
+    ref = O.protected_layer(dims, D, W, B, True, True, 1e-3, O_conv=Os)
+    got = r.verdict()
+    for k in ("detected", "stage", "stages_attempted"):
+        assert got[k] == ref[k], (t, k, got, ref)
+print("fused ok")
+"""
+
+
+@pytest.mark.gpu
+def test_fused_detect_path_verdict_parity():
+    env = dict(os.environ, FTC_FUSED_DETECT="1")
+    code = _FUSED_SCRIPT.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
