@@ -91,12 +91,18 @@ typedef struct ftc_plan {
  * targets use n = 0.
  * A negative coordinate means "all" along that axis (output_block/row/column).
  * Modes: BITFLIP flips bit (bit % 31) of the FP32 word (fault.hpp:82-87; on the
- * FP64 checksums bit % 63); ADD adds value + n_coef*n + m_coef*m; SET stores value. */
+ * FP64 checksums bit % 63); ADD adds value + n_coef*n + m_coef*m; SET stores value;
+ * SCALE is the reference's `perturb` (fault.hpp:72-80): v += T(mag_k * max(1, |v|)),
+ * mag_k = 0.5 + 1.5 * u_k with u_k the k-th uniform_real_distribution<double>(0, 1)
+ * draw of mt19937_64(seed), k = the element's row-major index over the fault's "all"
+ * (negative) axes -- make_hooks' iteration order (fault.hpp:111-172). */
 typedef enum ftc_fault_target {
   FTC_FAULT_OUTPUT = 0, FTC_FAULT_FMAP = 1, FTC_FAULT_KERNEL = 2,
   FTC_FAULT_CD1 = 3, FTC_FAULT_CD2 = 4, FTC_FAULT_CW1 = 5, FTC_FAULT_CW2 = 6
 } ftc_fault_target;
-typedef enum ftc_fault_mode { FTC_FAULT_BITFLIP = 0, FTC_FAULT_ADD = 1, FTC_FAULT_SET = 2 } ftc_fault_mode;
+typedef enum ftc_fault_mode {
+  FTC_FAULT_BITFLIP = 0, FTC_FAULT_ADD = 1, FTC_FAULT_SET = 2, FTC_FAULT_SCALE = 3
+} ftc_fault_mode;
 typedef struct ftc_fault {
   int32_t target;
   int32_t mode;
@@ -104,6 +110,7 @@ typedef struct ftc_fault {
   uint32_t bit;
   float value;
   float n_coef, m_coef;
+  uint64_t seed;  /* SCALE: the FaultSpec seed (fault.hpp:53) */
 } ftc_fault;
 
 /* LayerReport, report.hpp:38-47, as POD (fixed-capacity vectors). */
@@ -189,6 +196,44 @@ int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
 int ftc_protected_conv_launch_ck(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
                                  const double* cd1, const double* cd2, const ftc_fault* faults,
                                  int32_t n_faults, void* stream);
+
+/* ---- Fault campaigns (fault.hpp:42-291, replay.hpp) -------------------------------
+ * FaultSpec as POD.  target: 0 output_block, 1 output_row, 2 output_column, 3 fmap,
+ * 4 kernel, 5 checksum; checksum: 0 none, 1 cd1, 2 cd2, 3 cw1, 4 cw2; x/y = -1: all;
+ * mode: 0 scale (additive perturbation from `seed`), 1 bitflip (`bit`). */
+typedef struct ftc_fault_spec {
+  int32_t layer_index;
+  int32_t target;
+  int32_t checksum;
+  int32_t mode;
+  int64_t i, j;
+  int64_t x, y;
+  uint32_t bit;
+  uint32_t pad_;
+  uint64_t seed;
+} ftc_fault_spec;
+typedef struct ftc_ground_truth {
+  int32_t benign;
+  int32_t expected_stage; /* ftc_stage */
+  int32_t output_diverges;
+} ftc_ground_truth;
+typedef struct ftc_layer_grid {
+  int64_t N, M, Ch, H, R; /* LayerGrid (fault.hpp:191-193) */
+} ftc_layer_grid;
+
+/* campaign(layers, n_runs, weights, seed) (fault.hpp:195-271): the reproducible corpus,
+ * bit-identical to the reference's (same generator and distributions); weights over
+ * {output_block, output_row, output_column, fmap, kernel, checksum}. */
+int ftc_campaign(const ftc_layer_grid* layers, int32_t n_layers, int64_t n_runs, const double* weights6,
+                 uint64_t seed, ftc_fault_spec* specs, ftc_ground_truth* truths);
+/* ground_truth(f, N, M) (fault.hpp:174-211) */
+int ftc_ground_truth_of(const ftc_fault_spec* spec, int64_t N, int64_t M, ftc_ground_truth* out);
+/* make_hooks(f) (fault.hpp:111-172) as device fault records (at most 1) */
+int ftc_spec_faults(const ftc_fault_spec* spec, ftc_fault* out, int32_t* n_out);
+/* conv_forward of a run the faults hit (pre_conv + post_conv), no ABFT: what a fault
+ * does to an unprotected run (replay_entry's above-threshold test, replay.hpp:84-101) */
+int ftc_conv_forward_faulted(ftc_layer* layer, const float* D, float* O, const ftc_fault* faults,
+                             int32_t n_faults, void* stream);
 
 /* Channel-last input staging for the TMA im2col engine (C % 32 == 0 layers): the layer
  * keeps an NHWC copy of its input that every launch refreshes from D.  A producer that

@@ -356,3 +356,55 @@ def ref_protected_layer_f32(d: Dims, D, W, bias=None, tau=1e-4):
     res = rep.as_dict()
     res["status"] = st
     return res, O
+
+
+# ----------------------------------------------------------------------------- fault campaigns
+class RefSpec(C.Structure):  # layout of ftc_fault_spec / ref_spec
+    _fields_ = [("layer_index", C.c_int32), ("target", C.c_int32), ("checksum", C.c_int32), ("mode", C.c_int32),
+                ("i", C.c_int64), ("j", C.c_int64), ("x", C.c_int64), ("y", C.c_int64), ("bit", C.c_uint32),
+                ("pad_", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class RefTruth(C.Structure):
+    _fields_ = [("benign", C.c_int32), ("expected_stage", C.c_int32), ("output_diverges", C.c_int32)]
+
+
+class RefGrid(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("N", "M", "Ch", "H", "R")]
+
+
+def ref_campaign(grids, n_runs, weights=(1, 1, 1, 1, 1, 1), seed=0):
+    """The reference's campaign() (fault.hpp:195-271): list of (spec fields dict, truth dict)."""
+    R_ = ref()
+    g = (RefGrid * len(grids))(*[RefGrid(*x) for x in grids])
+    specs = (RefSpec * max(1, n_runs))()
+    truths = (RefTruth * max(1, n_runs))()
+    w = (C.c_double * 6)(*weights)
+    R_.ref_campaign.argtypes = [C.POINTER(RefGrid), C.c_int, C.c_longlong, C.POINTER(C.c_double), C.c_uint64,
+                                C.POINTER(RefSpec), C.POINTER(RefTruth)]
+    code = R_.ref_campaign(g, len(grids), n_runs, w, seed, specs, truths)
+    if code:
+        raise RuntimeError(f"ref_campaign failed ({code})")
+    out = []
+    for r in range(n_runs):
+        s, t = specs[r], truths[r]
+        out.append(({k: getattr(s, k) for k, _ in RefSpec._fields_ if k != "pad_"},
+                    {k: getattr(t, k) for k, _ in RefTruth._fields_}))
+    return out
+
+
+def ref_apply_spec(spec: dict, N, C_, H, M, R, E, D=None, W=None, O=None, cd1=None, cd2=None, cw1=None, cw2=None):
+    """make_hooks(f) of the reference applied to copies of the given host tensors (float
+    D/W/O; FP64 checksums); returns the perturbed copies in the same order."""
+    R_ = ref()
+    s = RefSpec(**spec)
+    cp = [None if a is None else np.ascontiguousarray(a).copy() for a in (D, W, O)]
+    ck = [None if a is None else np.ascontiguousarray(a, np.float64).copy() for a in (cd1, cd2, cw1, cw2)]
+    fp = lambda a: None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
+    dp = lambda a: None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+    R_.ref_apply_spec.argtypes = [C.POINTER(RefSpec)] + [C.c_int] * 6 + [C.POINTER(C.c_float)] * 3 + \
+        [C.POINTER(C.c_double)] * 4
+    code = R_.ref_apply_spec(C.byref(s), N, C_, H, M, R, E, *[fp(a) for a in cp], *[dp(a) for a in ck])
+    if code:
+        raise RuntimeError(f"ref_apply_spec failed ({code})")
+    return cp + ck

@@ -39,6 +39,19 @@ struct ref_report {
   double max_rel_dev;
 };
 
+struct ref_spec {  // layout of ftc_fault_spec
+  int32_t layer_index, target, checksum, mode;
+  int64_t i, j, x, y;
+  uint32_t bit, pad_;
+  uint64_t seed;
+};
+struct ref_truth {
+  int32_t benign, expected_stage, output_diverges;
+};
+struct ref_grid {
+  int64_t N, M, Ch, H, R;
+};
+
 struct ref_pre_fault {
   int target;  // 0=D 1=W 2=cd1 3=cd2 4=cw1 5=cw2
   long long index;
@@ -327,3 +340,107 @@ long long ref_locate_index(double r, int n) {
 int ref_values_differ(double c, double s, double tau) { return values_differ(c, s, tau) ? 1 : 0; }
 
 }  // extern "C"
+
+// ---- fault campaigns: the reference's own corpus generator and hooks (test oracle)
+namespace {
+FaultSpec to_spec(const ref_spec& r) {
+  FaultSpec f;
+  f.layer_index = static_cast<std::size_t>(r.layer_index);
+  f.target = static_cast<FaultTarget>(r.target);
+  f.checksum = static_cast<ChecksumName>(r.checksum);
+  f.i = static_cast<std::size_t>(r.i);
+  f.j = static_cast<std::size_t>(r.j);
+  f.x = r.x;
+  f.y = r.y;
+  f.mode = r.mode == 1 ? FaultMode::bitflip : FaultMode::scale;
+  f.bit = r.bit;
+  f.seed = r.seed;
+  return f;
+}
+}  // namespace
+
+extern "C" {
+
+// campaign (fault.hpp:195-271) + ground_truth
+int ref_campaign(const ref_grid* grids, int n_layers, long long n_runs, const double* w6, std::uint64_t seed,
+                 ref_spec* specs, ref_truth* truths) {
+  try {
+    std::vector<LayerGrid> layers;
+    for (int k = 0; k < n_layers; ++k)
+      layers.push_back(LayerGrid{(std::size_t)grids[k].N, (std::size_t)grids[k].M, (std::size_t)grids[k].Ch,
+                                 (std::size_t)grids[k].H, (std::size_t)grids[k].R});
+    TargetWeights w;
+    w.output_block = w6[0];
+    w.output_row = w6[1];
+    w.output_column = w6[2];
+    w.fmap = w6[3];
+    w.kernel = w6[4];
+    w.checksum = w6[5];
+    const auto corpus = campaign(layers, (std::size_t)n_runs, w, seed);
+    for (std::size_t r = 0; r < corpus.size(); ++r) {
+      const FaultSpec& f = corpus[r].fault;
+      ref_spec o{};
+      o.layer_index = (int32_t)f.layer_index;
+      o.target = (int32_t)f.target;
+      o.checksum = (int32_t)f.checksum;
+      o.mode = f.mode == FaultMode::bitflip ? 1 : 0;
+      o.i = (int64_t)f.i;
+      o.j = (int64_t)f.j;
+      o.x = f.x;
+      o.y = f.y;
+      o.bit = f.bit;
+      o.seed = f.seed;
+      specs[r] = o;
+      truths[r].benign = corpus[r].truth.benign;
+      truths[r].expected_stage = (int32_t)corpus[r].truth.expected_stage;
+      truths[r].output_diverges = corpus[r].truth.output_diverges;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// make_hooks<float>(f) applied to host tensors D (N,C,H,H), W (M,C,R,R), O (N,M,E,E) and
+// make_hooks<double>(f) to the FP64 checksums cd1/cd2 (1,C,H,H), cw1/cw2 (1,C,R,R); any
+// pointer may be null (that phase is skipped)
+int ref_apply_spec(const ref_spec* spec, int N, int C, int H, int M, int R, int E, float* D, float* W, float* O,
+                   double* cd1, double* cd2, double* cw1, double* cw2) {
+  try {
+    const FaultSpec f = to_spec(*spec);
+    FaultHooks<float> hf = make_hooks<float>(f);
+    if (O && hf.post_conv) {
+      auto Ot = make<float>(N, M, E, E, O);
+      hf.post_conv(Ot);
+      std::memcpy(O, Ot.data(), Ot.size() * sizeof(float));
+    }
+    if ((D || W) && hf.pre_conv && (f.target == FaultTarget::fmap || f.target == FaultTarget::kernel)) {
+      auto Dt = make<float>(D ? N : 1, C, H, H, D);
+      auto Wt = make<float>(W ? M : 1, C, R, R, W);
+      InputChecksums<float> ic;
+      hf.pre_conv(Dt, Wt, ic);
+      if (D) std::memcpy(D, Dt.data(), Dt.size() * sizeof(float));
+      if (W) std::memcpy(W, Wt.data(), Wt.size() * sizeof(float));
+    }
+    if (f.target == FaultTarget::checksum) {
+      FaultHooks<double> hd = make_hooks<double>(f);
+      Tensor4<double> Dd(1, 1, 1, 1), Wd(1, 1, 1, 1);
+      InputChecksums<double> ic;
+      ic.cd1 = make<double>(1, C, H, H, cd1);
+      ic.cd2 = make<double>(1, C, H, H, cd2);
+      ic.cw1 = make<double>(1, C, R, R, cw1);
+      ic.cw2 = make<double>(1, C, R, R, cw2);
+      hd.pre_conv(Dd, Wd, ic);
+      if (cd1) std::memcpy(cd1, ic.cd1.data(), ic.cd1.size() * sizeof(double));
+      if (cd2) std::memcpy(cd2, ic.cd2->data(), ic.cd2->size() * sizeof(double));
+      if (cw1) std::memcpy(cw1, ic.cw1.data(), ic.cw1.size() * sizeof(double));
+      if (cw2) std::memcpy(cw2, ic.cw2->data(), ic.cw2->size() * sizeof(double));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+}  // extern "C"
+

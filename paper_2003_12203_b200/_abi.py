@@ -25,6 +25,7 @@ EXPORTS = (
     "ftc_glue_act_pool", "ftc_glue_add_act", "ftc_glue_pad_crop", "ftc_protected_conv_launch_ck",
     "ftc_glue_act_pool_ck", "ftc_conv_forward_host", "ftc_protected_check",
     "ftc_layer_input_nhwc", "ftc_layer_input_nhwc_ready", "ftc_glue_act_pool_nhwc",
+    "ftc_campaign", "ftc_ground_truth_of", "ftc_spec_faults", "ftc_conv_forward_faulted",
 )
 
 
@@ -41,7 +42,21 @@ class Plan(C.Structure):
 class Fault(C.Structure):
     _fields_ = [("target", C.c_int32), ("mode", C.c_int32), ("n", C.c_int32), ("m", C.c_int32),
                 ("x", C.c_int32), ("y", C.c_int32), ("bit", C.c_uint32), ("value", C.c_float),
-                ("n_coef", C.c_float), ("m_coef", C.c_float)]
+                ("n_coef", C.c_float), ("m_coef", C.c_float), ("seed", C.c_uint64)]
+
+
+class FaultSpec(C.Structure):
+    _fields_ = [("layer_index", C.c_int32), ("target", C.c_int32), ("checksum", C.c_int32), ("mode", C.c_int32),
+                ("i", C.c_int64), ("j", C.c_int64), ("x", C.c_int64), ("y", C.c_int64), ("bit", C.c_uint32),
+                ("pad_", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class GroundTruth(C.Structure):
+    _fields_ = [("benign", C.c_int32), ("expected_stage", C.c_int32), ("output_diverges", C.c_int32)]
+
+
+class LayerGrid(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("N", "M", "Ch", "H", "R")]
 
 
 class Report(C.Structure):
@@ -98,6 +113,11 @@ def lib():
         L.ftc_glue_act_pool_nhwc.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
         L.ftc_layer_input_nhwc.argtypes = [vp, C.POINTER(vp)]
         L.ftc_layer_input_nhwc_ready.argtypes = [vp, vp]
+        L.ftc_campaign.argtypes = [C.POINTER(LayerGrid), i32, C.c_int64, C.POINTER(dbl), C.c_uint64,
+                                   C.POINTER(FaultSpec), C.POINTER(GroundTruth)]
+        L.ftc_ground_truth_of.argtypes = [C.POINTER(FaultSpec), C.c_int64, C.c_int64, C.POINTER(GroundTruth)]
+        L.ftc_spec_faults.argtypes = [C.POINTER(FaultSpec), C.POINTER(Fault), C.POINTER(i32)]
+        L.ftc_conv_forward_faulted.argtypes = [vp, vp, vp, C.POINTER(Fault), i32, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         _lib = L

@@ -70,9 +70,30 @@ __device__ __forceinline__ float flip_bit_f32(float v, unsigned bit) {
   return __uint_as_float(__float_as_uint(v) ^ (1u << (bit % 31u)));
 }
 
-// post_conv fault applied to one output element (inside conv epilogues)
-__device__ __forceinline__ float apply_output_faults(float v, int n, int m, int x, int y,
-                                                     const ftc_fault* f, int nf) {
+// Row-major index of element (a0..a3) over the fault's "all" (negative) axes, the
+// iteration order of the reference's make_hooks loops (fault.hpp:111-172).
+__device__ __forceinline__ long long fault_elem_index(const ftc_fault& f, int a0, int a1, int a2, int a3, int d1,
+                                                      int d2, int d3) {
+  long long k = 0;
+  if (f.n < 0) k = a0;
+  if (f.m < 0) k = k * d1 + a1;
+  if (f.x < 0) k = k * d2 + a2;
+  if (f.y < 0) k = k * d3 + a3;
+  return k;
+}
+
+// the reference's perturb: v += T(mag * max(1, |v|)) (fault.hpp:76-80), exact roundings
+__device__ __forceinline__ float scale_f32(float v, double mag) {
+  return __fadd_rn(v, (float)__dmul_rn(mag, fmax(1.0, fabs((double)v))));
+}
+__device__ __forceinline__ double scale_f64(double v, double mag) {
+  return __dadd_rn(v, __dmul_rn(mag, fmax(1.0, fabs(v))));
+}
+
+// post_conv fault applied to one output element (inside conv epilogues); tab holds the
+// SCALE magnitudes (the device record's `bit` is its offset into tab)
+__device__ __forceinline__ float apply_output_faults(float v, int n, int m, int x, int y, int M, int E,
+                                                     const ftc_fault* f, int nf, const double* tab) {
   for (int q = 0; q < nf; ++q) {
     const ftc_fault& a = f[q];
     if (a.target != FTC_FAULT_OUTPUT) continue;
@@ -83,6 +104,8 @@ __device__ __forceinline__ float apply_output_faults(float v, int n, int m, int 
       v = flip_bit_f32(v, a.bit);
     else if (a.mode == FTC_FAULT_ADD)
       v = v + (a.value + a.n_coef * (float)n + a.m_coef * (float)m);
+    else if (a.mode == FTC_FAULT_SCALE)
+      v = scale_f32(v, tab[a.bit + fault_elem_index(a, n, m, x, y, M, E, E)]);
     else
       v = a.value;
   }
@@ -118,6 +141,7 @@ struct ConvArgs {
   int N, C, H, M, R, U, pad, groups, E, Ckw;
   const ftc_fault* faults;  // device list (post_conv OUTPUT faults), may be null
   int nfaults;
+  const double* scale_tab;  // SCALE fault magnitudes (see apply_output_faults)
   double* rowsum;    // [N][E2] sum_m O (So2 before bias adjust), may be null
   double* rowsum_m;  // [N][E2] sum_m m*O (So4 before bias adjust), may be null
   const uint32_t* plane_mask;  // N*M bits: store only these planes (repair); null = all
@@ -240,7 +264,7 @@ int run_rollback(const Patches& p, int np_host, int M, int E2, const VerifyWS& w
 // plane mask (N*M bits) from the patch list
 int run_patch_planes(const Patches& p, int np_host, int M, uint32_t* mask, cudaStream_t s);
 // pre_conv faults on a float or double target
-int run_apply_faults(const ftc_fault* f_dev, int nf, int target, void* t, bool is_f64, int d1,
+int run_apply_faults(const ftc_fault* f_dev, int nf, int target, void* t, bool is_f64, const double* tab, int d1,
                      int d2, int d3, long long count, cudaStream_t s);
 
 }  // namespace ftc

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kPix) k_conv_simt(ConvArgs a) {
       if (m >= M || !valid) continue;
       float v = acc[q];
       if (a.bias) v = v + a.bias[m];
-      if (a.nfaults) v = apply_output_faults(v, n, m, x, y, a.faults, a.nfaults);
+      if (a.nfaults) v = apply_output_faults(v, n, m, x, y, a.M, a.E, a.faults, a.nfaults, a.scale_tab);
       const long long oi = ((long long)n * M + m) * E2 + f;
       bool store = true;
       if (a.plane_mask) {

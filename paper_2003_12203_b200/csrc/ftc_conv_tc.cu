@@ -98,6 +98,7 @@ struct TcArgs {
   long long P;     // N*E*E
   const ftc_fault* faults;
   int nfaults;
+  const double* scale_tab;
   double* rowsum;    // [2*ntiles][N*E2] or null (one slab per column half)
   double* rowsum_m;  // [2*ntiles][N*E2]
   const uint32_t* plane_mask;
@@ -234,9 +235,9 @@ struct HookOut {
   int store;
 };
 __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int y, const ftc_fault* f, int nf,
-                                               const uint32_t* plane_mask, int M) {
+                                               const uint32_t* plane_mask, int M, int E, const double* tab) {
   HookOut h;
-  h.v = nf ? apply_output_faults(v, n, m, x, y, f, nf) : v;
+  h.v = nf ? apply_output_faults(v, n, m, x, y, M, E, f, nf, tab) : v;
   h.store = 1;
   if (plane_mask) {
     const long long pl = (long long)n * M + m;
@@ -701,7 +702,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
                 if (bp) val = val + __ldg(bp + j);
                 int st = 1;
                 if (hooks) {
-                  const HookOut h = epilogue_hooks(val, n, m0 + j, x, y, a.faults, a.nfaults, a.plane_mask, a.M);
+                  const HookOut h =
+                      epilogue_hooks(val, n, m0 + j, x, y, a.faults, a.nfaults, a.plane_mask, a.M, E, a.scale_tab);
                   val = h.v;
                   st = h.store;
                 }
@@ -1115,6 +1117,7 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   if (a.npt <= 0) return FTC_OK;
   a.faults = c.faults;
   a.nfaults = c.nfaults;
+  a.scale_tab = c.scale_tab;
   a.rowsum = c.rowsum;
   a.rowsum_m = c.rowsum_m;
   a.plane_mask = c.plane_mask;

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <random>
+#include <vector>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -76,6 +78,8 @@ struct ftc_layer {
   ftc_fault* faults_dev = nullptr;
   ftc_fault* faults_h = nullptr;  // pinned staging
   int faults_cap = 0;
+  double* scale_tab = nullptr;    // SCALE fault magnitudes (device)
+  size_t scale_cap = 0;
   float* D_work = nullptr;
   float *D_host_buf = nullptr, *O_host_buf = nullptr;  // device buffers for the _host API
 
@@ -163,6 +167,7 @@ int run_conv(ftc_layer* L, const float* D, const float* W, float* O, bool faults
   a.Ckw = L->Ckw;
   a.faults = faults ? L->faults_dev : nullptr;
   a.nfaults = faults ? L->nfaults : 0;
+  a.scale_tab = L->scale_tab;
   a.rowsum = sums ? L->rowsum : nullptr;
   a.rowsum_m = sums ? L->rowsum_m : nullptr;
   a.plane_mask = plane_mask;
@@ -275,6 +280,7 @@ void free_layer(ftc_layer* L) {
   if (L->fstats_h) cudaFreeHost(L->fstats_h);
   F(L->fstats);
   F(L->fticket);
+  F(L->scale_tab);
   if (L->faults_h) cudaFreeHost(L->faults_h);
   if (L->res_h) cudaFreeHost(L->res_h);
   if (L->iscratch_h) cudaFreeHost(L->iscratch_h);
@@ -524,8 +530,8 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
   if (!L->ck_exact) {
     CK(launch_input_checksums(L->D, d.N, L->nCd, L->cd1, L->cd2, e.s));
     if (L->has_cd_faults) {
-      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, e.s));
-      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, e.s));
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, L->scale_tab, d.C, d.H, d.H, L->nCd, e.s));
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, L->scale_tab, d.C, d.H, d.H, L->nCd, e.s));
     }
     L->ck_exact = true;
   }
@@ -667,6 +673,44 @@ int stage_faults(ftc_layer* L, const ftc_fault* faults, int n, cudaStream_t s) {
   // the pinned staging buffer may still feed an earlier async copy
   FTC_CUDA_CHECK(cudaStreamSynchronize(s));
   std::memcpy(L->faults_h, faults, n * sizeof(ftc_fault));
+  // SCALE faults: expand the reference's per-element magnitudes on the host with the
+  // same generator and distribution (mt19937_64(seed), uniform_real_distribution
+  // <double>(0, 1), mag = 0.5 + 1.5 u, fault.hpp:76-80) in make_hooks' iteration order;
+  // the device record's `bit` carries the fault's offset into the table
+  {
+    std::vector<double> tab;
+    const ftc_conv_desc& d = L->d;
+    for (int q = 0; q < n; ++q) {
+      ftc_fault& f = L->faults_h[q];
+      if (f.mode != FTC_FAULT_SCALE) continue;
+      long long dims[4];
+      switch (f.target) {
+        case FTC_FAULT_OUTPUT: dims[0] = d.N; dims[1] = d.M; dims[2] = L->E; dims[3] = L->E; break;
+        case FTC_FAULT_FMAP: dims[0] = d.N; dims[1] = d.C; dims[2] = d.H; dims[3] = d.H; break;
+        case FTC_FAULT_KERNEL: dims[0] = d.M; dims[1] = L->Ckw; dims[2] = d.R; dims[3] = d.R; break;
+        case FTC_FAULT_CD1: case FTC_FAULT_CD2: dims[0] = 1; dims[1] = d.C; dims[2] = d.H; dims[3] = d.H; break;
+        default: dims[0] = 1; dims[1] = d.C; dims[2] = d.R; dims[3] = d.R; break;
+      }
+      const int coord[4] = {f.n, f.m, f.x, f.y};
+      long long count = 1;
+      for (int a = 0; a < 4; ++a) {
+        if (coord[a] >= dims[a]) RET_ERR(FTC_CONFIG_ERROR, "fault coordinates out of range");
+        if (coord[a] < 0) count *= dims[a];
+      }
+      f.bit = (uint32_t)tab.size();
+      std::mt19937_64 rng(f.seed);
+      std::uniform_real_distribution<double> u(0.0, 1.0);
+      for (long long k = 0; k < count; ++k) tab.push_back(0.5 + 1.5 * u(rng));
+    }
+    if (!tab.empty()) {
+      if (tab.size() > L->scale_cap) {
+        if (L->scale_tab) cudaFree(L->scale_tab);
+        L->scale_cap = tab.size();
+        CK(dalloc(&L->scale_tab, L->scale_cap));
+      }
+      FTC_CUDA_CHECK(cudaMemcpy(L->scale_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+  }
   FTC_CUDA_CHECK(cudaMemcpyAsync(L->faults_dev, L->faults_h, n * sizeof(ftc_fault), cudaMemcpyHostToDevice, s));
   L->nfaults = n;
   for (int q = 0; q < n; ++q)
@@ -794,6 +838,35 @@ int ftc_conv_forward(ftc_layer* L, const float* D, float* O, void* stream) {
   return timed_conv(L, D, L->W, O, false, false, (cudaStream_t)stream);
 }
 
+int ftc_conv_forward_faulted(ftc_layer* L, const float* D, float* O, const ftc_fault* faults, int32_t n_faults,
+                             void* stream) {
+  if (!L || !D || !O) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "a protected call is in flight on this layer");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(stage_faults(L, faults, n_faults, s));
+  const ftc_conv_desc& d = L->d;
+  const float* Dc = D;
+  const float* Wc = L->W;
+  if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_FMAP)) {
+    if (!L->D_work) CK(dalloc(&L->D_work, L->nD));
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->D_work, D, L->nD * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_FMAP, L->D_work, false, L->scale_tab, d.C, d.H, d.H,
+                        L->nD, s));
+    Dc = L->D_work;
+  }
+  if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_KERNEL)) {
+    if (!L->W_work) CK(dalloc(&L->W_work, L->nW));
+    FTC_CUDA_CHECK(cudaMemcpyAsync(L->W_work, L->W, L->nW * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_KERNEL, L->W_work, false, L->scale_tab, L->Ckw, d.R,
+                        d.R, L->nW, s));
+    Wc = L->W_work;
+  }
+  const int st = run_conv(L, Dc, Wc, O, L->n_out_faults > 0, false, nullptr, 0, d.N, s);
+  L->nfaults = 0;
+  L->n_out_faults = 0;
+  return st;
+}
+
 int ftc_conv_forward_host(ftc_layer* L, const float* D_host, float* O_host, void* stream) {
   if (!L || !D_host || !O_host) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
@@ -866,14 +939,14 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_FMAP)) {
     if (!L->D_work) CK(dalloc(&L->D_work, L->nD));
     FTC_CUDA_CHECK(cudaMemcpyAsync(L->D_work, D, L->nD * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_FMAP, L->D_work, false, d.C, d.H, d.H,
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_FMAP, L->D_work, false, L->scale_tab, d.C, d.H, d.H,
                         L->nD, s));
     L->Dconv = L->D_work;
   }
   if (L->nfaults && has_target(faults, n_faults, FTC_FAULT_KERNEL)) {
     if (!L->W_work) CK(dalloc(&L->W_work, L->nW));
     FTC_CUDA_CHECK(cudaMemcpyAsync(L->W_work, L->W, L->nW * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_KERNEL, L->W_work, false, L->Ckw, d.R,
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_KERNEL, L->W_work, false, L->scale_tab, L->Ckw, d.R,
                         d.R, L->nW, s));
     L->Wcur = L->W_work;
   }
@@ -882,8 +955,8 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   if (cwf) {
     FTC_CUDA_CHECK(cudaMemcpyAsync(L->cw1w, L->cw1g, L->nCw * sizeof(double), cudaMemcpyDeviceToDevice, s));
     FTC_CUDA_CHECK(cudaMemcpyAsync(L->cw2w, L->cw2g, L->nCw * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CW1, L->cw1w, true, d.C, d.R, d.R, L->nCw, s));
-    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CW2, L->cw2w, true, d.C, d.R, d.R, L->nCw, s));
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CW1, L->cw1w, true, L->scale_tab, d.C, d.R, d.R, L->nCw, s));
+    CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CW2, L->cw2w, true, L->scale_tab, d.C, d.R, d.R, L->nCw, s));
     L->cw1 = L->cw1w;
     L->cw2 = L->cw2w;
   }
@@ -944,9 +1017,9 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
       L->ck_exact = true;
     }
     if (L->has_cd_faults) {
-      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, d.C, d.H, d.H, L->nCd, L->side));
+      CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD1, L->cd1, true, L->scale_tab, d.C, d.H, d.H, L->nCd, L->side));
       if (L->ck_exact)
-        CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, d.C, d.H, d.H, L->nCd, L->side));
+        CK(run_apply_faults(L->faults_dev, L->nfaults, FTC_FAULT_CD2, L->cd2, true, L->scale_tab, d.C, d.H, d.H, L->nCd, L->side));
     }
   }
   CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, L->side));

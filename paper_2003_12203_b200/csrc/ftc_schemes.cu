@@ -380,7 +380,7 @@ __global__ void k_patch_planes(Patches p, int np, int M, uint32_t* mask) {
 // pre_conv faults on a 4-D target (d0 implied) -- fault.hpp:138-168 semantics
 template <typename T>
 __global__ void k_apply_faults(const ftc_fault* fl, int nf, int target, T* t, int d1, int d2,
-                               int d3, long long count) {
+                               int d3, long long count, const double* tab) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < count;
        e += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(e % d3), b = (int)((e / d3) % d2), a1 = (int)((e / ((long long)d3 * d2)) % d1);
@@ -402,6 +402,12 @@ __global__ void k_apply_faults(const ftc_fault* fl, int nf, int target, T* t, in
         }
       } else if (f.mode == FTC_FAULT_ADD) {
         v = v + (T)(f.value + f.n_coef * (float)a0 + f.m_coef * (float)a1);
+      } else if (f.mode == FTC_FAULT_SCALE) {
+        const double mag = tab[f.bit + fault_elem_index(f, a0, a1, b, c, d1, d2, d3)];
+        if (sizeof(T) == 4)
+          v = (T)scale_f32((float)v, mag);
+        else
+          v = (T)scale_f64((double)v, mag);
       } else {
         v = (T)f.value;
       }
@@ -490,14 +496,14 @@ int run_patch_planes(const Patches& p, int np, int M, uint32_t* mask, cudaStream
   return FTC_OK;
 }
 
-int run_apply_faults(const ftc_fault* f_dev, int nf, int target, void* t, bool is_f64, int d1,
+int run_apply_faults(const ftc_fault* f_dev, int nf, int target, void* t, bool is_f64, const double* tab, int d1,
                      int d2, int d3, long long count, cudaStream_t s) {
   if (is_f64)
     FTC_LAUNCH(k_apply_faults<double><<<grid_for(count), kT, 0, s>>>(f_dev, nf, target, (double*)t, d1, d2,
-                                                          d3, count));
+                                                          d3, count, tab));
   else
     FTC_LAUNCH(k_apply_faults<float><<<grid_for(count), kT, 0, s>>>(f_dev, nf, target, (float*)t, d1, d2, d3,
-                                                         count));
+                                                         count, tab));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -117,7 +117,7 @@ class LayerReport:
 
 # ----------------------------------------------------------------------------- faults (fault.hpp)
 TARGETS = {"output": 0, "fmap": 1, "kernel": 2, "cd1": 3, "cd2": 4, "cw1": 5, "cw2": 6}
-MODES = {"bitflip": 0, "add": 1, "set": 2}
+MODES = {"bitflip": 0, "add": 1, "set": 2, "scale": 3}
 
 
 @dataclass
@@ -133,10 +133,11 @@ class Fault:
     value: float = 0.0
     n_coef: float = 0.0
     m_coef: float = 0.0
+    seed: int = 0  # scale mode: the FaultSpec seed (mt19937_64 magnitudes, fault.hpp:72-80)
 
     def c(self) -> _abi.Fault:
         return _abi.Fault(TARGETS[self.target], MODES[self.mode], self.n, self.m, self.x, self.y,
-                          self.bit, self.value, self.n_coef, self.m_coef)
+                          self.bit, self.value, self.n_coef, self.m_coef, self.seed & (2**64 - 1))
 
 
 def output_bitflip(n, m, x, y, bit) -> Fault:

@@ -45,7 +45,7 @@ def test_extent_rule_without_gpu():
 
 def test_fault_struct_layout_matches_header():
     from paper_2003_12203_b200 import _abi
-    assert C.sizeof(_abi.Fault) == 40
+    assert C.sizeof(_abi.Fault) == 48
     assert C.sizeof(_abi.ConvDesc) == 36
     assert C.sizeof(_abi.Plan) == 48
 
