@@ -152,6 +152,8 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
                      ftc_layer** out);
 int ftc_layer_destroy(ftc_layer* layer);
 int ftc_layer_extent(const ftc_layer* layer, int32_t* E);
+/* the geometry the layer was created with */
+int ftc_layer_desc(const ftc_layer* layer, ftc_conv_desc* desc);
 
 /* conv_forward(D, W, bias, p) (conv.hpp:114-131) with the layer's golden W. */
 int ftc_conv_forward(ftc_layer* layer, const float* D, float* O, void* stream);
@@ -234,6 +236,35 @@ int ftc_spec_faults(const ftc_fault_spec* spec, ftc_fault* out, int32_t* n_out);
  * does to an unprotected run (replay_entry's above-threshold test, replay.hpp:84-101) */
 int ftc_conv_forward_faulted(ftc_layer* layer, const float* D, float* O, const ftc_fault* faults,
                              int32_t n_faults, void* stream);
+
+/* ---- Layer plans (workflow.hpp:19-112, 428-501) ------------------------------------ */
+typedef struct ftc_layer_dims {
+  int64_t N, M, Ch, H, R, E; /* LayerDims (workflow.hpp:38-40) */
+} ftc_layer_dims;
+typedef struct ftc_plan_info {  /* LayerPlan with its profiled runtimes (workflow.hpp:22-28) */
+  int32_t rc_enabled, clc_enabled;
+  double tau;
+  double t0, t1, t2; /* CoC+FC, CoC+RC, CoC+RC+FC */
+  double p_r;
+} ftc_plan_info;
+typedef struct ftc_profile_result {  /* ProfileResult (workflow.hpp:423-427) */
+  double rc_t0, rc_t1, rc_t2;
+  double clc_t0, clc_t1, clc_t2;
+  int32_t used_cost_model;
+} ftc_profile_result;
+/* scheme: 0 coc_d, 1 coc, 2 rc, 3 clc, 4 fc (schemes.hpp:15) */
+double ftc_cost_model(int32_t scheme, const ftc_layer_dims* dims, double alpha, double beta);
+int32_t ftc_decide_rc(double t0, double t1, double t2, double p_r, double p_c);
+int32_t ftc_decide_clc(double t0, double t1, double t2, double p_r, double p_c);
+void ftc_estimate_error_probs(const ftc_layer_dims* dims, double* p_r, double* p_c);
+/* make_default_plan(dims, tau, {alpha, beta}) (workflow.hpp:99-112) */
+int ftc_make_default_plan(const ftc_layer_dims* dims, double tau, double alpha, double beta, ftc_plan_info* out);
+/* profile_layer (workflow.hpp:428-501) on the device path: the protected layer timed
+ * (host wall clock, median of `reps`) under the six forced-fault variants -- a row fault
+ * O(1,m,.,.) += 3 + m and a column fault O(n,1,.,.) += 3 + n -- falling back to the
+ * cost model for degenerate layers (N < 2 or M < 2) or non-positive times. */
+int ftc_profile_layer(ftc_layer* layer, const float* D, double tau, int32_t reps, ftc_profile_result* out,
+                      void* stream);
 
 /* Channel-last input staging for the TMA im2col engine (C % 32 == 0 layers): the layer
  * keeps an NHWC copy of its input that every launch refreshes from D.  A producer that

@@ -408,3 +408,37 @@ def ref_apply_spec(spec: dict, N, C_, H, M, R, E, D=None, W=None, O=None, cd1=No
     if code:
         raise RuntimeError(f"ref_apply_spec failed ({code})")
     return cp + ck
+
+
+def ref_plan_to_json(plans: dict) -> str:
+    """The reference's plan_to_json (serialize.cpp:115-124); plans: name -> dict with
+    rc_enabled, clc_enabled, tau, t0, t1, t2, p_r."""
+    R_ = ref()
+    names = list(plans)
+    arr_n = (C.c_char_p * max(1, len(names)))(*[n.encode() for n in names])
+    vals = []
+    for n in names:
+        p = plans[n]
+        vals += [float(p["rc_enabled"]), float(p["clc_enabled"]), p["tau"], p["t0"], p["t1"], p["t2"], p["p_r"]]
+    v = (C.c_double * max(1, len(vals)))(*vals)
+    buf = C.create_string_buffer(1 << 20)
+    R_.ref_plan_to_json.argtypes = [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.c_char_p, C.c_longlong]
+    R_.ref_plan_to_json.restype = C.c_longlong
+    n = R_.ref_plan_to_json(len(names), arr_n, v, buf, len(buf))
+    if n < 0:
+        raise RuntimeError("ref_plan_to_json failed")
+    return buf.value.decode()
+
+
+def ref_corpus_to_jsonl(entries) -> str:
+    """The reference's corpus_to_jsonl (serialize.cpp:68-80); entries: (spec dict, truth dict)."""
+    R_ = ref()
+    specs = (RefSpec * max(1, len(entries)))(*[RefSpec(**s) for s, _ in entries])
+    truths = (RefTruth * max(1, len(entries)))(*[RefTruth(**t) for _, t in entries])
+    buf = C.create_string_buffer(1 << 22)
+    R_.ref_corpus_to_jsonl.argtypes = [C.c_int, C.POINTER(RefSpec), C.POINTER(RefTruth), C.c_char_p, C.c_longlong]
+    R_.ref_corpus_to_jsonl.restype = C.c_longlong
+    n = R_.ref_corpus_to_jsonl(len(entries), specs, truths, buf, len(buf))
+    if n < 0:
+        raise RuntimeError("ref_corpus_to_jsonl failed")
+    return buf.value.decode()

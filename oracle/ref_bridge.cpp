@@ -18,6 +18,7 @@
 #include "ftconv/conv.hpp"
 #include "ftconv/fault.hpp"
 #include "ftconv/schemes.hpp"
+#include "ftconv/serialize.hpp"
 #include "ftconv/workflow.hpp"
 
 using namespace ftconv;
@@ -439,6 +440,57 @@ int ref_apply_spec(const ref_spec* spec, int N, int C, int H, int M, int R, int 
     return 0;
   } catch (const std::exception& e) {
     return code_of(e);
+  }
+}
+
+}  // extern "C"
+
+// ---- file formats (serialize.cpp): plan and corpus text, for byte-level pins
+extern "C" {
+
+// plan_to_json over n named plans {rc, clc, tau, t0, t1, t2, p_r}; returns the length
+// written into out (cap bytes) or -1
+long long ref_plan_to_json(int n, const char* const* names, const double* vals7, char* out, long long cap) {
+  try {
+    std::map<std::string, LayerPlan> plans;
+    for (int k = 0; k < n; ++k) {
+      LayerPlan p;
+      p.rc_enabled = vals7[7 * k + 0] != 0;
+      p.clc_enabled = vals7[7 * k + 1] != 0;
+      p.tau = vals7[7 * k + 2];
+      p.t0 = vals7[7 * k + 3];
+      p.t1 = vals7[7 * k + 4];
+      p.t2 = vals7[7 * k + 5];
+      p.p_r = vals7[7 * k + 6];
+      plans[names[k]] = p;
+    }
+    const std::string t = plan_to_json(plans);
+    if ((long long)t.size() + 1 > cap) return -1;
+    std::memcpy(out, t.c_str(), t.size() + 1);
+    return (long long)t.size();
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// corpus_to_jsonl of n (spec, truth) pairs
+long long ref_corpus_to_jsonl(int n, const ref_spec* specs, const ref_truth* truths, char* out, long long cap) {
+  try {
+    std::vector<CorpusEntry> es;
+    for (int k = 0; k < n; ++k) {
+      CorpusEntry e;
+      e.fault = to_spec(specs[k]);
+      e.truth.benign = truths[k].benign != 0;
+      e.truth.expected_stage = static_cast<ResolveStage>(truths[k].expected_stage);
+      e.truth.output_diverges = truths[k].output_diverges != 0;
+      es.push_back(e);
+    }
+    const std::string t = corpus_to_jsonl(es);
+    if ((long long)t.size() + 1 > cap) return -1;
+    std::memcpy(out, t.c_str(), t.size() + 1);
+    return (long long)t.size();
+  } catch (const std::exception&) {
+    return -1;
   }
 }
 

@@ -26,6 +26,8 @@ EXPORTS = (
     "ftc_glue_act_pool_ck", "ftc_conv_forward_host", "ftc_protected_check",
     "ftc_layer_input_nhwc", "ftc_layer_input_nhwc_ready", "ftc_glue_act_pool_nhwc",
     "ftc_campaign", "ftc_ground_truth_of", "ftc_spec_faults", "ftc_conv_forward_faulted",
+    "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
+    "ftc_profile_layer", "ftc_layer_desc",
 )
 
 
@@ -57,6 +59,20 @@ class GroundTruth(C.Structure):
 
 class LayerGrid(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("N", "M", "Ch", "H", "R")]
+
+
+class LayerDims(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("N", "M", "Ch", "H", "R", "E")]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("rc_enabled", C.c_int32), ("clc_enabled", C.c_int32), ("tau", C.c_double), ("t0", C.c_double),
+                ("t1", C.c_double), ("t2", C.c_double), ("p_r", C.c_double)]
+
+
+class ProfileResult(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("rc_t0", "rc_t1", "rc_t2", "clc_t0", "clc_t1", "clc_t2")] + \
+        [("used_cost_model", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -118,6 +134,15 @@ def lib():
         L.ftc_ground_truth_of.argtypes = [C.POINTER(FaultSpec), C.c_int64, C.c_int64, C.POINTER(GroundTruth)]
         L.ftc_spec_faults.argtypes = [C.POINTER(FaultSpec), C.POINTER(Fault), C.POINTER(i32)]
         L.ftc_conv_forward_faulted.argtypes = [vp, vp, vp, C.POINTER(Fault), i32, vp]
+        L.ftc_cost_model.argtypes = [i32, C.POINTER(LayerDims), dbl, dbl]
+        L.ftc_cost_model.restype = dbl
+        L.ftc_decide_rc.argtypes = [dbl] * 5
+        L.ftc_decide_clc.argtypes = [dbl] * 5
+        L.ftc_estimate_error_probs.argtypes = [C.POINTER(LayerDims), C.POINTER(dbl), C.POINTER(dbl)]
+        L.ftc_estimate_error_probs.restype = None
+        L.ftc_make_default_plan.argtypes = [C.POINTER(LayerDims), dbl, dbl, dbl, C.POINTER(PlanInfo)]
+        L.ftc_profile_layer.argtypes = [vp, vp, dbl, i32, C.POINTER(ProfileResult), vp]
+        L.ftc_layer_desc.argtypes = [vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         _lib = L

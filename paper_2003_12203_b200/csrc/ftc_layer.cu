@@ -838,6 +838,12 @@ int ftc_conv_forward(ftc_layer* L, const float* D, float* O, void* stream) {
   return timed_conv(L, D, L->W, O, false, false, (cudaStream_t)stream);
 }
 
+int ftc_layer_desc(const ftc_layer* L, ftc_conv_desc* desc) {
+  if (!L || !desc) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  *desc = L->d;
+  return FTC_OK;
+}
+
 int ftc_conv_forward_faulted(ftc_layer* L, const float* D, float* O, const ftc_fault* faults, int32_t n_faults,
                              void* stream) {
   if (!L || !D || !O) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
