@@ -347,6 +347,78 @@ class ProtectedNet:
             L.close()
 
 
+class HostPipeline:
+    """Host-buffer inference over a ProtectedNet with the copies overlapped.
+
+    Each batch is copied in from (pinned) host memory and its result copied back, as
+    with a serial ``set_input -> forward -> output`` loop, but batch k+1's H2D runs on a
+    copy stream under batch k's protected forward (two device input slots), and batch
+    k's result leaves through a device staging copy and an async D2H on a second copy
+    stream.  Verdicts are read per batch (``ProtectedNet.finish``) before the next batch
+    is launched, so repairs and replays behave exactly as in ``forward``."""
+
+    def __init__(self, pn: ProtectedNet):
+        torch = pn.torch
+        self.pn, self.torch = pn, torch
+        self.slots = [pn.buf["x"], torch.empty_like(pn.buf["x"])]
+        out = pn.output()
+        self.stage = [torch.empty_like(out), torch.empty_like(out)]
+        self.s_in = torch.cuda.Stream(device=out.device)
+        self.s_out = torch.cuda.Stream(device=out.device)
+
+    def run(self, xs_host, outs_host, before_step=None, start_event=None, faults=None):
+        """xs_host[k] -> outs_host[k] for every k; returns the per-batch verdict dicts.
+        ``before_step`` is called on the compute stream ahead of each batch (bench.py's L2
+        flush); ``start_event`` (recorded on the compute stream) gates the first H2D."""
+        torch, pn = self.torch, self.pn
+        main = torch.cuda.current_stream()
+        Ev = torch.cuda.Event
+        ev_in, ev_used, ev_staged, ev_out = [Ev(), Ev()], [None, None], [Ev(), Ev()], [None, None]
+        if start_event is not None:
+            self.s_in.wait_event(start_event)
+
+        def h2d(k):
+            s = k % 2
+            if ev_used[s] is not None:  # the batch two back has finished with this slot
+                self.s_in.wait_event(ev_used[s])
+            with torch.cuda.stream(self.s_in):
+                self.slots[s].copy_(xs_host[k], non_blocking=True)
+            ev_in[s].record(self.s_in)
+
+        reps = []
+        K = len(xs_host)
+        if K:
+            h2d(0)
+        for k in range(K):
+            s = k % 2
+            if k + 1 < K:
+                h2d(k + 1)
+            main.wait_event(ev_in[s])
+            if before_step is not None:
+                before_step()
+            pn.buf["x"] = self.slots[s]
+            pn.launch(faults, main)
+            reps.append(pn.finish(main))
+            used = Ev()
+            used.record(main)
+            ev_used[s] = used
+            if ev_out[s] is not None:  # the D2H two batches back has drained this stage
+                main.wait_event(ev_out[s])
+            self.stage[s].copy_(pn.output(), non_blocking=True)
+            ev_staged[s].record(main)
+            self.s_out.wait_event(ev_staged[s])
+            with torch.cuda.stream(self.s_out):
+                outs_host[k].copy_(self.stage[s], non_blocking=True)
+            done = Ev()
+            done.record(self.s_out)
+            ev_out[s] = done
+        for e in ev_out:
+            if e is not None:
+                main.wait_event(e)
+        pn.buf["x"] = self.slots[0]
+        return reps
+
+
 def calibrate_taus(net, batch, seed, dev, factor=4.0):
     """tau_L per layer: >= 4x the max fault-free FP64 residual over all
     seven families of the FP32 output, rounded up to a power of ten."""
@@ -410,6 +482,15 @@ class BenchNet:
         self.out_host.copy_(self.pn.output(), non_blocking=True)
         self.pn.torch.cuda.current_stream().synchronize()
         return list(reps.values())
+
+    def e2e_stream(self, steps, before_step=None, start_event=None):
+        """`steps` host batches through HostPipeline (H2D/D2H overlapped with compute)."""
+        if not hasattr(self, "pipe"):
+            self.pipe = HostPipeline(self.pn)
+            self.outs_host = [self.out_host, self.pn.torch.empty_like(self.out_host).pin_memory()]
+        reps = self.pipe.run([self.x_host] * steps, [self.outs_host[k % 2] for k in range(steps)],
+                             before_step, start_event)
+        return [list(r.values()) for r in reps]
 
 
 # ----------------------------------------------------------------------------- CPU reference

@@ -136,3 +136,32 @@ def test_net_layer_verdict_matches_oracle():
             assert got[k] == ref[k], (r, k, got, ref)
         assert [tuple(t) for t in got["corrected_blocks"]] == [tuple(t) for t in ref["corrected_blocks"]]
     pn.close()
+
+
+def test_host_pipeline_matches_serial_forward():
+    """HostPipeline (H2D of batch k+1 under batch k, staged D2H) returns, per batch,
+    bitwise the output and the verdicts of a serial set_input -> forward -> output."""
+    import paper_2003_12203_b200 as F
+    torch = _torch()
+    net, pn = build("alexnet", 2)
+    xs = [torch.from_numpy(nets.net_input(net, 2, s)).pin_memory() for s in (5, 6, 7, 8, 9)]
+    want = []
+    for x in xs:
+        pn.set_input(x.cuda())
+        reps = pn.forward()
+        want.append((pn.output().cpu().clone(), {k: r.stage for k, r in reps.items()}))
+    pipe = nets.HostPipeline(pn)
+    outs = [torch.empty(pn.output().shape).pin_memory() for _ in xs]
+    got = pipe.run(xs, outs)
+    torch.cuda.synchronize()
+    for k, (o, reps) in enumerate(zip(outs, got)):
+        assert torch.equal(o, want[k][0]), k
+        assert {n: r.stage for n, r in reps.items()} == want[k][1]
+    # a fault in a middle layer: every batch is repaired and its output is the clean one
+    faults = {"c3": [F.output_bitflip(1, 7, 2, 3, 27)]}
+    got = pipe.run(xs[:3], outs[:3], faults=faults)
+    torch.cuda.synchronize()
+    for k in range(3):
+        assert got[k]["c3"].detected
+        assert torch.equal(outs[k], want[k][0]), k
+    pn.close()
