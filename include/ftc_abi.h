@@ -198,6 +198,13 @@ int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
 int ftc_protected_conv_launch_ck(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
                                  const double* cd1, const double* cd2, const ftc_fault* faults,
                                  int32_t n_faults, void* stream);
+/* _launch with only the clean-path input checksum supplied by the producer of D:
+ * cd1 = sum_n D_n in FP64 in any order (ftc_glue_act_pool_cd1 writes it at the
+ * start of its workspace).  CoC-D needs nothing else; the exact-order Cd1/Cd2
+ * (checksums.hpp:100-107) are recomputed from D only if CoC-D fires. */
+int ftc_protected_conv_launch_cd1(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                                  const double* cd1, const ftc_fault* faults, int32_t n_faults,
+                                  void* stream);
 
 /* ---- Fault campaigns (fault.hpp:42-291, replay.hpp) -------------------------------
  * FaultSpec as POD.  target: 0 output_block, 1 output_row, 2 output_column, 3 fmap,
@@ -330,6 +337,14 @@ int ftc_glue_act_pool_ck(const float* in, float* out, int32_t N, int32_t C, int3
 int ftc_glue_act_pool_nhwc(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
                            int32_t act, int32_t k, int32_t s, int32_t p, double* cd1, double* cd2,
                            void* stream);
+/* ftc_glue_act_pool(_nhwc) that also writes, with ws != NULL, the next protected
+ * layer's clean-path Cd1 = sum_n out_n (FP64, any order) into ws[0 : C*Ho*Ho] -- pass
+ * ws to ftc_protected_conv_launch_cd1.  ws holds ftc_glue_ws_doubles(...) doubles
+ * (Cd1, per-image-group partial slabs, tickets) and must be zero-filled once before
+ * first use; the kernels leave it re-armed.  out_nhwc may be NULL. */
+int64_t ftc_glue_ws_doubles(int32_t N, int32_t C, int32_t H, int32_t k, int32_t s, int32_t p);
+int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
+                          int32_t act, int32_t k, int32_t s, int32_t p, double* ws, void* stream);
 /* out = act(a + b) elementwise over n values (b may be NULL) */
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act,
                      void* stream);

@@ -27,7 +27,8 @@ EXPORTS = (
     "ftc_layer_input_nhwc", "ftc_layer_input_nhwc_ready", "ftc_glue_act_pool_nhwc",
     "ftc_campaign", "ftc_ground_truth_of", "ftc_spec_faults", "ftc_conv_forward_faulted",
     "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
-    "ftc_profile_layer", "ftc_layer_desc",
+    "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
+    "ftc_protected_conv_launch_cd1",
 )
 
 
@@ -144,6 +145,10 @@ def lib():
         L.ftc_profile_layer.argtypes = [vp, vp, dbl, i32, C.POINTER(ProfileResult), vp]
         L.ftc_layer_desc.argtypes = [vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
+        L.ftc_glue_ws_doubles.argtypes = [i32] * 6
+        L.ftc_glue_ws_doubles.restype = C.c_int64
+        L.ftc_glue_act_pool_cd1.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]
+        L.ftc_protected_conv_launch_cd1.argtypes = [vp, C.POINTER(Plan), vp, vp, vp, C.POINTER(Fault), i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         _lib = L
     return _lib

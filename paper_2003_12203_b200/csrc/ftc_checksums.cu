@@ -413,6 +413,68 @@ __global__ void __launch_bounds__(256) k_detect_adapt(const double* __restrict__
   }
 }
 
+// Co5 tap table of the fused clean path: k = (c*R + i)*R + j (the conv_block order)
+__global__ void k_co5_taps(const double* __restrict__ cw1, int C, int H, int R, Co5Tap* taps) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= C * R * R) return;
+  const int c = k / (R * R), ij = k % (R * R), i = ij / R, j = ij % R;
+  Co5Tap t;
+  t.off = c * H * H + i * H + j;
+  t.i = (short)i;
+  t.j = (short)j;
+  t.w = cw1[k];
+  taps[k] = t;
+}
+
+// CoC-D of the fused clean path: So5 was accumulated by the conv epilogue (FP64 atomics,
+// bias not yet removed), Co5 by its checksum warp.  One thread per position compares
+// them (values_differ, checksums.hpp:54-60) and re-zeroes So5; the last block publishes
+// {flagged, max_rel_dev} into the mapped host record and re-arms the counters.
+__global__ void __launch_bounds__(256) k_detect_fused(const double* __restrict__ co5, double* __restrict__ so5,
+                                                     int N, int E2, int bias, const double* agg, double tau,
+                                                     DetectStats* st, unsigned int* ticket, DetectStats* host_out) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  int bad = 0;
+  unsigned long long devb = 0ull;
+  if (f < E2) {
+    double ss = __ldcg(so5 + f);
+    so5[f] = 0.0;
+    if (bias) ss -= (double)N * agg[0];
+    const double c = __ldcg(co5 + f);
+    double den = fabs(c);
+    if (den < fabs(ss)) den = fabs(ss);
+    if (den < 1.0) den = 1.0;
+    const double dev = fabs(c - ss) / den;
+    if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
+    bad = values_differ(c, ss, tau) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+    devb = other > devb ? other : devb;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(&st->flagged, bad);
+    if (devb) atomicMax(&st->max_rel_dev_bits, devb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(ticket, 1u);
+    if (done == gridDim.x - 1) {
+      __threadfence();
+      const int fl = atomicExch(&st->flagged, 0);
+      const unsigned long long mb = atomicExch(&st->max_rel_dev_bits, 0ull);
+      volatile DetectStats* h = host_out;
+      h->flagged = fl;
+      h->max_rel_dev_bits = mb;
+      __threadfence_system();
+      *ticket = 0u;
+    }
+  }
+}
+
 inline int pick_positions(int work_per_position) {
   // slices S ~ work/4 (a few serial steps per thread), P = 256 / S positions per block
   int S = 16;
@@ -433,6 +495,13 @@ int launch_input_checksums(const float* D, int N, long long per, double* cd1, do
     FTC_LAUNCH(k_input_checksums_v4<<<blocks_for(per / 4), kThreads, 0, s>>>(D, N, per / 4, cd1, cd2));
   else
     FTC_LAUNCH(k_input_checksums_scalar<<<blocks_for(per), kThreads, 0, s>>>(D, N, per, cd1, cd2));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_co5_taps(const double* cw1, int C, int H, int R, Co5Tap* taps, cudaStream_t s) {
+  if (R > 32767 || (long long)C * H * H >= (1LL << 31)) return FTC_CONFIG_ERROR;
+  FTC_LAUNCH(k_co5_taps<<<blocks_for((long long)C * R * R), kThreads, 0, s>>>(cw1, C, H, R, taps));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -520,6 +589,14 @@ int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N,
   const int P = pick_positions(N * parts);
   FTC_LAUNCH(k_detect_adapt<<<(E2 + P - 1) / P, 256, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st, ticket,
                                                              host_out, P));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
+                        DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s) {
+  FTC_LAUNCH(k_detect_fused<<<blocks_for(E2), kThreads, 0, s>>>(co5, so5, N, E2, bias, agg, tau, st, ticket,
+                                                                host_out));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

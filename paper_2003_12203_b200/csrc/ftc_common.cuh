@@ -122,8 +122,15 @@ struct DetectStats {
 // Clean-path CoC-D fused into the tcgen05 conv (TMA im2col engine): Co5 = Cd1 (x) Cw1 is
 // computed before the conv; the conv adds its pixels' row sums into So5 (FP64 atomics)
 // and its last CTA compares them and publishes the record.
+struct Co5Tap {  // one (c, i, j) term of Co5 = Cd1 (*) Cw1
+  int off;         // c*H*H + i*H + j
+  short i, j;
+  double w;        // Cw1[c][i][j]
+};
+
 struct FusedDetect {
-  double* co5;            // [E2], computed before the conv
+  double* co5;            // [E2]: written by the conv's checksum warp when cdp != null,
+                          // else computed before the conv
   double* so5;            // [E2] accumulator: zero on entry, re-zeroed by the last CTA
   const double* agg;      // bias aggregates (agg[0] = sum_m B[m])
   double tau;
@@ -131,6 +138,10 @@ struct FusedDetect {
   DetectStats* st;        // device counters, zero on entry, re-zeroed
   unsigned int* ticket;   // zero on entry, re-zeroed
   DetectStats* host_out;  // mapped host record
+  // in-kernel Co5 = Cd1 (*) Cw1 (tcgen05 engine, checksum warps), or null when co5 is
+  // precomputed
+  const double* cd1;      // [C][H][H]
+  const Co5Tap* taps;     // [C*R*R] per-tap offsets and Cw1 values
 };
 
 struct ConvArgs {
@@ -160,6 +171,7 @@ bool tc_supported(const ftc_conv_desc& d);
 int conv_tc_launch(const TcPlan* p, const ConvArgs& a, cudaStream_t s);
 int tc_rowsum_parts(const TcPlan* p);
 bool tc_im2col(const TcPlan* p);           // TMA im2col engine (fused detection available)
+bool tc_co5_in_kernel(const TcPlan* p, int N, int E);  // fused path: Co5 by the conv's checksum warp
 float* tc_nhwc_buffer(const TcPlan* p);    // its NHWC input copy
 // D (NCHW) -> Dt (NHWC) for images [n_lo, n_lo + nimg); with cd1 != null also the exact
 // input checksums Cd1/Cd2 (n ascending, FP64; whole batch only: n_lo = 0, nimg = N)
@@ -193,6 +205,17 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
 // clean path: Cd1 only, parallel over positions (FTC_CONFIG_ERROR when the plane size
 // is odd -> caller uses the exact kernel)
 int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStream_t s);
+// clean path: Cd1 = sum_n D_n in FP64, any order, through a workspace [Cd1][tickets]
+// [partial slabs over image groups] (zero-filled once; the kernels re-arm the tickets).
+// The act+pool glue kernels write the next layer's Cd1 the same way.
+int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
+                        DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s);
+int launch_co5_taps(const double* cw1, int C, int H, int R, Co5Tap* taps, cudaStream_t s);
+long long cd1_ws_doubles(int N, long long per);
+// C, Ho: the pooling producer's shape when the workspace is shared with it (0, 0: none)
+int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStream_t s, int C = 0, int Ho = 0);
+int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k, int s,
+                         int p, cudaStream_t st);
 // clean path: Co5 (adaptive positions x channel slices), then So5 from the fused row
 // sums + compare; the last block publishes the record into mapped host memory
 // (host_out) and re-zeroes st/ticket for the next call

@@ -21,7 +21,10 @@
 //   warps 11-18 epilogue (two per TMEM lane quarter, each owning half of the BN
 //               columns): drain the accumulator every G K-chunks into register sums,
 //               then + bias, post_conv faults, coalesced NCHW store, fused FP64 row sums
-//               (So2/So4 partials).
+//               (So2/So4 partials);
+//   warp 19     (FUSE) checksum warp: Co5 = Cd1 (*) Cw1 at this CTA's share of the
+//               output positions, in the shadow of the MMAs; the epilogue adds its row
+//               sums into So5 (FP64 atomics); a small kernel after the conv runs CoC-D.
 //
 // Why the drain: the tensor core aligns every addend to the accumulator's exponent
 // and drops the bits below its ulp, so one accumulator over the whole K loses
@@ -82,7 +85,15 @@ constexpr int kLoaderWarp = 8;
 constexpr int kMmaWarp = 9;  // and 10: two issuers alternating K chunks
 constexpr int kEpiWarp0 = 11;
 constexpr int kEpiThreads = 256;
-constexpr int kThreads = 608;
+// fused clean path: one checksum warp computes Co5 = Cd1 (*) Cw1 at this CTA's positions
+// (a 21st warp would put 6 warps on one SM sub-partition and cap registers at 80)
+constexpr int kCkWarp0 = 19;
+constexpr int kCkWarps = 1;
+#ifndef FTC_CK_UNROLL
+#define FTC_CK_UNROLL 8
+#endif
+constexpr int kCkUnroll = FTC_CK_UNROLL;  // taps in flight per lane
+constexpr int kThreads = 640;
 
 struct TcArgs {
   const float* D;
@@ -102,8 +113,7 @@ struct TcArgs {
   double* rowsum;    // [2*ntiles][N*E2] or null (one slab per column half)
   double* rowsum_m;  // [2*ntiles][N*E2]
   const uint32_t* plane_mask;
-  FusedDetect fd;  // valid when fuse != 0 (MODE 2)
-  int fuse;
+  FusedDetect fd;  // valid for FUSE instantiations
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -247,12 +257,13 @@ __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int
 }
 
 // MODE 0: NCHW im2col gather by the producers; 1: NHWC gather (4 x 16-byte loads per
-// chunk); 2: TMA im2col into shared memory, producers only split and store to TMEM
-template <int BN, int MODE>
+// chunk); 2: TMA im2col into shared memory, producers only split and store to TMEM.
+// FUSE: clean-path CoC-D operands inside the kernel: the checksum warp computes Co5, the
+// epilogue adds its row sums into So5; launch_detect_fused compares them afterwards.
+template <int BN, int MODE, bool FUSE>
 __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_constant__ CUtensorMap tmA) {
   constexpr bool NHWC = MODE == 1;
   constexpr bool TMAA = MODE >= 2;
-  constexpr bool FUSE = MODE == 3;  // TMA im2col + fused clean-path CoC-D
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the B stages (SW128 atoms)
   const uint32_t raw = smem_u32(smem_raw);
@@ -588,6 +599,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         }
       }
     }
+  } else if (warp >= kCkWarp0) {
+    // ================= checksum warps (FUSE) =================
+    // Co5[f] = sum_{c,i,j} Cd1[c][x*U+i-pad][y*U+j-pad] * Cw1[c][i][j] (conv_block,
+    // checksums.hpp:135-145, FP64; zero padding) for f = blockIdx.x + k*gridDim.x: lanes
+    // split the taps (kCkUnroll loads in flight each), a shuffle tree sums them.  The
+    // compare runs in the next launch on the stream, which sees every store.
+    // (The compare used to be the last CTA's job here; its code in the kernel pushed
+    // the epilogue's drain loop into register spills: ~12% on the conv.)
+    if constexpr (FUSE) {
+      if (a.fd.cd1 && !(a.dbg & 8192)) {
+        const int Kt = a.C * RR;
+        const int cw = warp - kCkWarp0;
+        for (int f = blockIdx.x + cw * gridDim.x; f < E2; f += kCkWarps * gridDim.x) {
+          const int x = f / E, y = f - (f / E) * E;
+          const int hb = x * a.U - a.pad, wb = y * a.U - a.pad;
+          const double* cd = a.fd.cd1 + hb * H + wb;
+          double acc = 0.0;
+          for (int k0 = 0; k0 < Kt; k0 += 32 * kCkUnroll) {
+            double v[kCkUnroll], w[kCkUnroll];
+#pragma unroll
+            for (int u = 0; u < kCkUnroll; ++u) {
+              const int k = k0 + u * 32 + lane;
+              v[u] = 0.0;
+              w[u] = 0.0;
+              if (k < Kt) {
+                const int4 t = __ldg(reinterpret_cast<const int4*>(a.fd.taps + k));
+                const int ti = t.y & 0xFFFF, tj = t.y >> 16;
+                if ((unsigned)(hb + ti) < (unsigned)H && (unsigned)(wb + tj) < (unsigned)H) {
+                  v[u] = __ldg(cd + t.x);
+                  w[u] = __hiloint2double(t.w, t.z);
+                }
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kCkUnroll; ++u) acc = fma(v[u], w[u], acc);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) a.fd.co5[f] = acc;
+        }
+      }
+    }
   } else {
     // ================= epilogue =================
     constexpr int HALF = BN / 2;  // columns owned by this warp
@@ -725,76 +778,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       }
       // fused CoC-D: So5 accumulates from the row sums (order-free FP64 atomics; the exact
       // families are recomputed in reference order if anything is flagged)
-      if (FUSE && valid) atomicAdd(a.fd.so5 + f, rs);
+      if (FUSE && valid && !(a.dbg & 4096)) atomicAdd(a.fd.so5 + f, rs);
       TC_TRACE(eprof, 9, tl);
-    }
-    if constexpr (FUSE) {
-      // fused CoC-D: the last CTA to finish compares So5 (bias adjusted) with Co5
-      // at every position (values_differ), publishes {flagged, max_rel_dev} into the
-      // mapped host record and re-zeroes So5 / counters / ticket for the next launch
-      volatile int& s_last = *reinterpret_cast<volatile int*>(tmem_slot + 1);  // dynamic smem
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-      const int et = (int)threadIdx.x - kEpiWarp0 * 32;
-      if (et == 0) {
-        if (!(a.dbg & 2048)) __threadfence();
-        s_last = atomicAdd(a.fd.ticket, 1u) == gridDim.x - 1;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-      if (s_last) {
-        __threadfence();
-        int bad = 0;
-        unsigned long long devb = 0ull;
-        for (int fb = et; fb < E2; fb += kEpiThreads * 8) {  // 8 positions' loads in flight
-          double sv[8], cv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int fp = fb + u * kEpiThreads;
-            sv[u] = fp < E2 ? __ldcg(a.fd.so5 + fp) : 0.0;
-            cv[u] = fp < E2 ? __ldcg(a.fd.co5 + fp) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int fp = fb + u * kEpiThreads;
-            if (fp >= E2) break;
-            a.fd.so5[fp] = 0.0;
-            double ss = sv[u];
-            if (a.fd.bias) ss -= (double)a.N * a.fd.agg[0];
-            const double c = cv[u];
-            double den = fabs(c);
-            if (den < fabs(ss)) den = fabs(ss);
-            if (den < 1.0) den = 1.0;
-            const double dev = fabs(c - ss) / den;
-            if (dev == dev && dev > 0.0) {
-              const unsigned long long b = (unsigned long long)__double_as_longlong(dev);
-              devb = b > devb ? b : devb;
-            }
-            bad += values_differ(c, ss, a.fd.tau) ? 1 : 0;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          bad += __shfl_xor_sync(0xffffffffu, bad, o);
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
-          devb = other > devb ? other : devb;
-        }
-        if (lane == 0) {
-          if (bad) atomicAdd(&a.fd.st->flagged, bad);
-          if (devb) atomicMax(&a.fd.st->max_rel_dev_bits, devb);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-        if (et == 0) {
-          __threadfence();
-          const int fl = atomicExch(&a.fd.st->flagged, 0);
-          const unsigned long long mb = atomicExch(&a.fd.st->max_rel_dev_bits, 0ull);
-          if (!(a.dbg & 1024)) {
-            volatile DetectStats* h = a.fd.host_out;
-            h->flagged = fl;
-            h->max_rel_dev_bits = mb;
-            __threadfence_system();
-          }
-          *a.fd.ticket = 0u;
-        }
-      }
     }
   }
   tc_before();
@@ -919,15 +904,15 @@ __global__ void __launch_bounds__(256) k_nhwc_cd(const float* __restrict__ D, fl
 
 int g_num_sms = 0;
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool FUSE>
 int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024));
     attr_set = true;
   }
-  FTC_LAUNCH(k_conv_tc<BN, MODE><<<grid, kThreads, smem, s>>>(a, tm));
+  FTC_LAUNCH(k_conv_tc<BN, MODE, FUSE><<<grid, kThreads, smem, s>>>(a, tm));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -1064,6 +1049,21 @@ void tc_plan_destroy(TcPlan* p) {
 
 int tc_rowsum_parts(const TcPlan* p) { return p ? 2 * p->ntiles : 1; }
 bool tc_im2col(const TcPlan* p) { return p && p->im2col; }
+
+// Whether the conv's single checksum warp finishes Co5 well inside the conv: its
+// latency rounds (one L2 round trip per kCkUnroll taps per lane, ~700 cycles) against
+// the CTA's MMA work (~1000 cycles per K chunk of a tile).  Small convs (config 1: 21
+// positions x 576 taps per CTA vs ~3 tiles x 18 chunks) take a separate Co5 kernel.
+bool tc_co5_in_kernel(const TcPlan* p, int N, int E) {
+  if (!p) return false;
+  const long long E2 = (long long)E * E;
+  const long long grid = 148;
+  const long long pos = (E2 + grid - 1) / grid;
+  const long long rounds = pos * ((p->K + 32LL * kCkUnroll - 1) / (32LL * kCkUnroll));
+  const long long tiles = ((long long)N * E2 + kBM - 1) / kBM * p->ntiles;
+  const long long conv = (tiles + grid - 1) / grid * p->nkc * 1000LL;
+  return rounds * 700LL * 4 <= conv;
+}
 float* tc_nhwc_buffer(const TcPlan* p) { return p ? p->Dt : nullptr; }
 
 int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg, double* cd1, double* cd2,
@@ -1151,44 +1151,35 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
     }
     a.D = p->Dt;
   }
-  a.fuse = 0;
-  if (c.fd) {
-    if (!p->im2col) {
-      set_error(FTC_CONFIG_ERROR, "fused detection needs the im2col engine");
+  const bool fuse = c.fd != nullptr;
+  if (fuse) {
+    if (p->nhwc) {
+      set_error(FTC_CONFIG_ERROR, "fused detection: not with the NHWC gather engine");
       return FTC_CONFIG_ERROR;
     }
     a.fd = *c.fd;
-    a.fuse = 1;
   }
-  if (p->im2col && a.fuse) {
-    switch (p->BN) {
-      case 32: return launch_bn<32, 3>(a, p->tmA, grid, smem, s);
-      case 64: return launch_bn<64, 3>(a, p->tmA, grid, smem, s);
-      case 96: return launch_bn<96, 3>(a, p->tmA, grid, smem, s);
-      case 128: return launch_bn<128, 3>(a, p->tmA, grid, smem, s);
-    }
-  } else if (p->im2col) {
-    switch (p->BN) {
-      case 32: return launch_bn<32, 2>(a, p->tmA, grid, smem, s);
-      case 64: return launch_bn<64, 2>(a, p->tmA, grid, smem, s);
-      case 96: return launch_bn<96, 2>(a, p->tmA, grid, smem, s);
-      case 128: return launch_bn<128, 2>(a, p->tmA, grid, smem, s);
+#define FTC_BN_SWITCH(MODE, FUSE)                                                  \
+  switch (p->BN) {                                                                 \
+    case 32: return launch_bn<32, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
+    case 64: return launch_bn<64, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
+    case 96: return launch_bn<96, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
+    case 128: return launch_bn<128, MODE, FUSE>(a, p->tmA, grid, smem, s);         \
+  }
+  if (p->im2col) {
+    if (fuse) {
+      FTC_BN_SWITCH(2, true)
+    } else {
+      FTC_BN_SWITCH(2, false)
     }
   } else if (p->nhwc) {
-    switch (p->BN) {
-      case 32: return launch_bn<32, 1>(a, p->tmA, grid, smem, s);
-      case 64: return launch_bn<64, 1>(a, p->tmA, grid, smem, s);
-      case 96: return launch_bn<96, 1>(a, p->tmA, grid, smem, s);
-      case 128: return launch_bn<128, 1>(a, p->tmA, grid, smem, s);
-    }
+    FTC_BN_SWITCH(1, false)
+  } else if (fuse) {
+    FTC_BN_SWITCH(0, true)
   } else {
-    switch (p->BN) {
-      case 32: return launch_bn<32, 0>(a, p->tmA, grid, smem, s);
-      case 64: return launch_bn<64, 0>(a, p->tmA, grid, smem, s);
-      case 96: return launch_bn<96, 0>(a, p->tmA, grid, smem, s);
-      case 128: return launch_bn<128, 0>(a, p->tmA, grid, smem, s);
-    }
+    FTC_BN_SWITCH(0, false)
   }
+#undef FTC_BN_SWITCH
   set_error(FTC_CONFIG_ERROR, "unsupported BN");
   return FTC_CONFIG_ERROR;
 }

@@ -137,6 +137,143 @@ __global__ void __launch_bounds__(256) k_act_pool_t(const float* __restrict__ in
   if (spos < plane) out_t[(n * plane + spos) * C + blockIdx.y * 32 + wc] = tile[wp][wc];
 }
 
+// Clean-path Cd1 = sum_n D_n (FP64, any order -- CoC-D is tolerance based; the error
+// path recomputes the exact-order checksums, checksums.hpp:100-107).  Workspace
+// [Cd1][G partial slabs][tickets], zero-filled once: block (x, g) sums image group g at
+// 256 positions (one per thread, 8 loads in flight), and the last group block of each x
+// folds the slabs into Cd1 (g ascending) and re-arms its ticket.
+// Workspace layout shared by the Cd1 producers (Cd1Ws): [Cd1: per][tickets][G slabs]
+struct Cd1Ws {
+  long long per;       // C * H * H
+  long long tick_off;  // in doubles
+  long long slab_off;  // in doubles
+  int tickets;
+};
+
+__device__ __forceinline__ unsigned int* ws_tickets(double* ws, long long tick_off) {
+  return reinterpret_cast<unsigned int*>(ws + tick_off);
+}
+
+// last of the G group blocks of a tile folds the slabs (g ascending) into Cd1 at
+// positions [e0, e0 + count) and re-arms the tile's ticket
+__device__ __forceinline__ bool ws_arrive(double* ws, long long tick_off, int tile, int G) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ws_tickets(ws, tick_off) + tile, 1u) == (unsigned)(G - 1);
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+__global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, int N, long long per, int NG,
+                                                  double* __restrict__ ws, long long tick_off, long long slab_off) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.y, G = gridDim.y;
+  const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
+  if (e < per) {
+    double a = 0.0;
+    int n = n_lo;
+    for (; n + 8 <= n_hi; n += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(D + (long long)(n + u) * per + e);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += (double)v[u];
+    }
+    for (; n < n_hi; ++n) a += (double)__ldcs(D + (long long)n * per + e);
+    ws[slab_off + per * g + e] = a;
+  }
+  if (ws_arrive(ws, tick_off, blockIdx.x, G)) {
+    if (e < per) {
+      double t = 0.0;
+      for (int gg = 0; gg < G; ++gg) t += __ldcg(ws + slab_off + per * gg + e);
+      ws[e] = t;
+    }
+    if (threadIdx.x == 0) ws_tickets(ws, tick_off)[blockIdx.x] = 0u;
+  }
+}
+
+// k_act_pool_t over a group of images per block, also summing each thread's (c, position)
+// over the group in FP64 into the Cd1 workspace (the consumer conv's clean-path Cd1)
+template <int KT>
+__global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict__ in, float* __restrict__ out,
+                                                       float* __restrict__ out_t, int N, int NG, int C, int H,
+                                                       int act, int kr, int s, int p, int Ho, double* __restrict__ ws,
+                                                       long long tick_off, long long slab_off) {
+  __shared__ float tile[8][33];
+  const int k = KT > 0 ? KT : kr;
+  const int plane = Ho * Ho;
+  const int tid = threadIdx.x;
+  const int cl = tid >> 3, pl = tid & 7;
+  const int c = blockIdx.y * 32 + cl, pos = blockIdx.x * 8 + pl;
+  const int wc = tid & 31, wp = tid >> 5;
+  const int spos = blockIdx.x * 8 + wp;
+  const int g = blockIdx.z, G = gridDim.z;
+  const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
+  const bool ok = pos < plane;
+  int x0 = 0, y0 = 0;
+  if (ok) {
+    const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
+    x0 = ox * s - p;
+    y0 = oy * s - p;
+  }
+  double acc = 0.0;
+  for (int n = n_lo; n < n_hi; ++n) {
+    float m = -INFINITY;
+    if (ok) {
+      const float* src = in + ((long long)n * C + c) * H * H;
+      if constexpr (KT > 0) {
+        float v[KT * KT];
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const int x = x0 + i, y = y0 + j;
+            v[i * KT + j] = (x >= 0 && x < H && y >= 0 && y < H) ? __ldg(src + x * H + y) : 0.f;
+          }
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            const int x = x0 + i, y = y0 + j;
+            if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[i * KT + j], act));
+          }
+      } else {
+        for (int i = 0; i < k; ++i) {
+          const int x = x0 + i;
+          if (x < 0 || x >= H) continue;
+          for (int j = 0; j < k; ++j) {
+            const int y = y0 + j;
+            if (y < 0 || y >= H) continue;
+            m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
+          }
+        }
+      }
+      out[((long long)n * C + c) * plane + pos] = m;
+      acc += (double)m;
+    }
+    if (out_t) {
+      tile[pl][cl] = m;
+      __syncthreads();
+      if (spos < plane) out_t[((long long)n * plane + spos) * C + blockIdx.y * 32 + wc] = tile[wp][wc];
+      __syncthreads();
+    }
+  }
+  const long long per = (long long)C * plane;
+  const long long e = (long long)c * plane + pos;
+  if (ok) ws[slab_off + per * g + e] = acc;
+  const int tl = blockIdx.y * gridDim.x + blockIdx.x;
+  if (ws_arrive(ws, tick_off, tl, G)) {
+    if (ok) {
+      double t = 0.0;
+      for (int gg = 0; gg < G; ++gg) t += __ldcg(ws + slab_off + per * gg + e);
+      ws[e] = t;
+    }
+    if (tid == 0) ws_tickets(ws, tick_off)[tl] = 0u;
+  }
+}
+
 int launch_act_pool(const float* in, float* out, int NC, int H, int act, int k, int s, int p, int Ho,
                     cudaStream_t st) {
   const int gy = (NC + 3) / 4;
@@ -179,6 +316,103 @@ inline int grid_for(long long n) {
 }
 
 }  // namespace
+
+// Image groups each Cd1 producer reduces separately (enough blocks to cover the SMs a
+// few times, at most 16 partial slabs) and the shared workspace layout
+int groups_for(int N, long long blocks_per_group) {
+  long long G = (16LL * 148 + blocks_per_group - 1) / blocks_per_group;
+  if (G > 16) G = 16;
+  if (G > N) G = N;
+  if (G < 1) G = 1;
+  const int NG = (int)((N + G - 1) / G);
+  return (N + NG - 1) / NG;  // no empty group
+}
+
+int cd1_parts_groups(int N, long long per) { return groups_for(N, (per + 255) / 256); }
+
+int act_pool_groups(int N, int C, int Ho) {
+  return groups_for(N, (long long)((Ho * Ho + 7) / 8) * ((C + 31) / 32));
+}
+
+// per = C*Ho*Ho; Ho = 0 when there is no pooling producer (k_cd1_parts only)
+Cd1Ws cd1_ws_layout(int N, int C, int Ho, long long per) {
+  Cd1Ws w{};
+  w.per = per;
+  long long t = (per + 255) / 256;
+  int G = cd1_parts_groups(N, per);
+  if (Ho > 0) {
+    const long long t2 = (long long)((Ho * Ho + 7) / 8) * ((C + 31) / 32);
+    t = t > t2 ? t : t2;
+    const int G2 = act_pool_groups(N, C, Ho);
+    G = G > G2 ? G : G2;
+  }
+  w.tickets = (int)t;
+  w.tick_off = per;
+  w.slab_off = per + (t + 1) / 2;
+  (void)G;
+  return w;
+}
+
+long long cd1_ws_doubles_g(int N, int C, int Ho, long long per) {
+  const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
+  int G = cd1_parts_groups(N, per);
+  if (Ho > 0) {
+    const int G2 = act_pool_groups(N, C, Ho);
+    G = G > G2 ? G : G2;
+  }
+  return w.slab_off + (long long)G * per;
+}
+
+long long cd1_ws_doubles(int N, long long per) { return cd1_ws_doubles_g(N, 0, 0, per); }
+
+int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k, int s,
+                         int p, cudaStream_t st) {
+  const int Ho = (H + 2 * p - k) / s + 1;
+  const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)N);
+  if (k == 3)
+    FTC_LAUNCH(k_act_pool_t<3><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
+  else if (k == 2)
+    FTC_LAUNCH(k_act_pool_t<2><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
+  else if (k == 1)
+    FTC_LAUNCH(k_act_pool_t<1><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
+  else
+    FTC_LAUNCH(k_act_pool_t<0><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStream_t st, int C, int Ho) {
+  const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
+  const int G = cd1_parts_groups(N, per);
+  const int NG = (N + G - 1) / G;
+  const dim3 g((unsigned)((per + 255) / 256), (unsigned)((N + NG - 1) / NG));
+  FTC_LAUNCH(k_cd1_parts<<<g, 256, 0, st>>>(D, N, per, NG, ws, w.tick_off, w.slab_off));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k,
+                             int s, int p, double* ws, cudaStream_t st) {
+  const int Ho = (H + 2 * p - k) / s + 1;
+  const long long per = (long long)C * Ho * Ho;
+  const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
+  const int G = act_pool_groups(N, C, Ho);
+  const int NG = (N + G - 1) / G;
+  const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
+#define FTC_APT(KT)                                                                                   \
+  FTC_LAUNCH(k_act_pool_t_cd1<KT><<<g, 256, 0, st>>>(in, out, out_t, N, NG, C, H, act, k, s, p, Ho, ws, \
+                                                      w.tick_off, w.slab_off))
+  switch (k) {
+    case 1: FTC_APT(1); break;
+    case 2: FTC_APT(2); break;
+    case 3: FTC_APT(3); break;
+    default: FTC_APT(0); break;
+  }
+#undef FTC_APT
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
 }  // namespace ftc
 
 using namespace ftc;
@@ -224,19 +458,39 @@ int ftc_glue_act_pool_nhwc(const float* in, float* out, float* out_nhwc, int32_t
     return FTC_CONFIG_ERROR;
   }
   const int Ho = (H + 2 * p - k) / s + 1;
-  const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)N);
   cudaStream_t st = (cudaStream_t)stream;
-  if (k == 3)
-    FTC_LAUNCH(k_act_pool_t<3><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
-  else if (k == 2)
-    FTC_LAUNCH(k_act_pool_t<2><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
-  else if (k == 1)
-    FTC_LAUNCH(k_act_pool_t<1><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
-  else
-    FTC_LAUNCH(k_act_pool_t<0><<<g, 256, 0, st>>>(in, out, out_nhwc, C, H, act, k, s, p, Ho));
-  FTC_CUDA_CHECK(cudaGetLastError());
+  {
+    const int rc = launch_act_pool_nhwc(in, out, out_nhwc, N, C, H, act, k, s, p, st);
+    if (rc != FTC_OK) return rc;
+  }
   if (!cd1) return FTC_OK;
   return launch_input_checksums(out, N, (long long)C * Ho * Ho, cd1, cd2, st);
+}
+
+int64_t ftc_glue_ws_doubles(int32_t N, int32_t C, int32_t H, int32_t k, int32_t s, int32_t p) {
+  if (N <= 0 || C <= 0 || k <= 0 || s <= 0 || p < 0 || H + 2 * p < k) return 0;
+  const int Ho = (H + 2 * p - k) / s + 1;
+  return cd1_ws_doubles_g(N, C, Ho, (long long)C * Ho * Ho);
+}
+
+int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
+                          int32_t act, int32_t k, int32_t s, int32_t p, double* ws, void* stream) {
+  if (k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || !in || !out || (out_nhwc && C % 32)) {
+    set_error(FTC_CONFIG_ERROR, "bad pooling window, null buffer or NHWC output with C % 32 != 0");
+    return FTC_CONFIG_ERROR;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int Ho = (H + 2 * p - k) / s + 1;
+  if (!ws) {
+    return out_nhwc ? launch_act_pool_nhwc(in, out, out_nhwc, N, C, H, act, k, s, p, st)
+                    : launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
+  }
+  // with the consumer's Cd1: channel-blocked kernel looping over image groups (one
+  // pass), or -- C not a multiple of 32 -- act + pool, then Cd1 from the L2-hot output
+  if (C % 32 == 0) return launch_act_pool_nhwc_cd1(in, out, out_nhwc, N, C, H, act, k, s, p, ws, st);
+  const int rc = launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
+  if (rc != FTC_OK) return rc;
+  return launch_cd1_parts(out, N, (long long)C * Ho * Ho, ws, st, C, Ho);
 }
 
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act, void* stream) {

@@ -66,6 +66,8 @@ struct ftc_layer {
   double *cd1 = nullptr, *cd2 = nullptr;
   double* co5f = nullptr;
   double* so5acc = nullptr;  // fused clean path: So5 accumulator (zero between calls)
+  Co5Tap* co5tab = nullptr;  // fused clean path: Co5 taps (offsets + golden Cw1)
+  double* cd1ws = nullptr;   // fused clean path: Cd1 workspace ([Cd1][slabs][tickets], zeroed)
   bool nhwc_ready = false;   // the next conv's NHWC input copy is already staged (one-shot)
   const float* D_staged = nullptr;  // the D it was staged from (set by the caller's next launch)
   double *rowsum = nullptr, *rowsum_m = nullptr;
@@ -267,7 +269,7 @@ void free_layer(ftc_layer* L) {
     if (p) cudaFree(p);
   };
   F(L->W); F(L->W_work); F(L->bias); F(L->agg); F(L->cw1g); F(L->cw2g); F(L->cw1w); F(L->cw2w);
-  F(L->cd1); F(L->cd2); F(L->co5f); F(L->so5acc); F(L->rowsum); F(L->rowsum_m); F(L->stats); F(L->faults_dev);
+  F(L->cd1); F(L->cd2); F(L->co5f); F(L->so5acc); F(L->co5tab); F(L->cd1ws); F(L->rowsum); F(L->rowsum_m); F(L->stats); F(L->faults_dev);
   F(L->D_work); F(L->D_host_buf); F(L->O_host_buf);
   for (int k = 0; k < 7; ++k) {
     F(L->cs[k]);
@@ -777,6 +779,12 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
       (st = dalloc(&L->so5acc, L->E2)) || (st = dalloc(&L->stats, 1)))
     return fail(st);
   if (cudaMemset(L->so5acc, 0, L->E2 * sizeof(double)) != cudaSuccess) return fail(FTC_CUDA_ERROR);
+  {
+    // Cd1 workspace of the fused clean path when no producer supplies Cd1
+    const long long n = cd1_ws_doubles(desc->N, L->nCd);
+    if ((st = dalloc(&L->cd1ws, (size_t)n)) || (st = dalloc(&L->co5tab, (size_t)L->nCw))) return fail(st);
+    if (cudaMemset(L->cd1ws, 0, (size_t)n * sizeof(double)) != cudaSuccess) return fail(FTC_CUDA_ERROR);
+  }
   if (cudaMallocHost((void**)&L->stats_h, sizeof(DetectStats)) != cudaSuccess)
     return fail(FTC_CUDA_ERROR);
   if ((st = dalloc(&L->fstats, 1)) || (st = dalloc(&L->fticket, 1))) return fail(st);
@@ -797,6 +805,7 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
   }
   if ((st = launch_kernel_checksums(L->W, desc->M, L->Ckw, desc->R, desc->groups, L->cw1g, L->cw2g, 0)))
     return fail(st);
+  if ((st = launch_co5_taps(L->cw1g, desc->C, desc->H, desc->R, L->co5tab, 0))) return fail(st);
   if (cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_start, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&L->ev_ck, cudaEventDisableTiming) != cudaSuccess ||
@@ -974,27 +983,43 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   const double* cd1_use = L->cd1;
   L->cd_ext1 = L->cd_ext2 = nullptr;
   const bool pre_faults = L->Dconv != D || L->Wcur != L->W || cwf || L->has_cd_faults;
-  // opt-in until it beats the side-stream path end to end (three dependent launches
-  // before the persistent conv cost more than the fusion saves)
-  static const bool fused_ok = getenv("FTC_FUSED_DETECT") != nullptr;
-  if (fused_ok && use_tc(L) && tc_im2col(L->tc) && !pre_faults) {
-    // Fused clean path (TMA im2col engine): one pre-pass writes the NHWC copy and, unless
-    // the producer of D already reduced it, the exact Cd1/Cd2; Co5 follows; the conv
-    // accumulates So5 from its row sums and its last CTA runs CoC-D -- no side stream,
-    // nothing launched after the persistent conv.
+  // Fused clean path (tcgen05 engine, golden operands): Cd1 comes from the producer
+  // (glue kernels) or one streaming pass over D (small batches: the same pass stages the
+  // NHWC copy for the TMA im2col engine); the conv computes Co5 in its checksum warp and
+  // accumulates So5 from its row sums; one small kernel then runs CoC-D.
+  static const bool fused_off = getenv("FTC_NO_FUSED") != nullptr;
+  if (!fused_off && use_tc(L) && !pre_faults) {
+    bool dt_ready = false;
     if (cd1_in) {
-      L->cd_ext1 = cd1_in;
-      L->cd_ext2 = cd2_in;
       cd1_use = cd1_in;
-      CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, nullptr, nullptr, s));
+      if (cd2_in) {  // exact-order checksums: kept for the error path
+        L->cd_ext1 = cd1_in;
+        L->cd_ext2 = cd2_in;
+        L->ck_exact = true;
+      } else {
+        L->ck_exact = false;
+      }
     } else {
-      CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s));
+      const bool stage = tc_im2col(L->tc) && !(L->nhwc_ready && L->D_staged == D);
+      if (stage && d.N <= 32) {
+        // small batch: one pass writes the NHWC copy and the exact-order Cd1/Cd2
+        CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s));
+        dt_ready = true;
+        cd1_use = L->cd1;
+        L->ck_exact = true;
+      } else {
+        CK(launch_cd1_parts(D, d.N, L->nCd, L->cd1ws, s));
+        cd1_use = L->cd1ws;
+        L->ck_exact = false;
+      }
     }
-    L->ck_exact = true;
-    CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, s));
+    const bool co5_in = tc_co5_in_kernel(L->tc, d.N, L->E);
+    if (!co5_in) CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, s));
     FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
-                   L->fstats_hd};
-    CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, true, s, &fd, true));
+                   L->fstats_hd, co5_in ? cd1_use : nullptr, L->co5tab};
+    CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready));
+    CK(launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats,
+                           L->fticket, L->fstats_hd, s));
     FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
     L->inflight = true;
     return FTC_OK;
@@ -1004,7 +1029,13 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, s));
   CK(timed_conv(L, L->Dconv, L->Wcur, O, L->n_out_faults > 0, true, s));
   FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
-  if (cd1_in && !L->has_cd_faults) {
+  if (cd1_in && !cd2_in) {  // producer Cd1 in any order (ftc_protected_conv_launch_cd1)
+    if (L->has_cd_faults) cd1_in = nullptr;  // checksum faults: reduce D here instead
+  }
+  if (cd1_in && !cd2_in) {
+    cd1_use = cd1_in;
+    L->ck_exact = false;
+  } else if (cd1_in && !L->has_cd_faults) {
     // read the producer's checksums in place; copied into the layer only if the
     // error path runs
     cd1_use = cd1_in;
@@ -1041,6 +1072,12 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
 int ftc_protected_conv_launch(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
                               const ftc_fault* faults, int32_t n_faults, void* stream) {
   return launch_impl(L, plan, D, O, nullptr, nullptr, faults, n_faults, stream);
+}
+
+int ftc_protected_conv_launch_cd1(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
+                                  const double* cd1, const ftc_fault* faults, int32_t n_faults, void* stream) {
+  if (!cd1) RET_ERR(FTC_INVALID_ARGUMENT, "null input checksum");
+  return launch_impl(L, plan, D, O, cd1, nullptr, faults, n_faults, stream);
 }
 
 int ftc_protected_conv_launch_ck(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,

@@ -283,6 +283,14 @@ class ProtectedConv:
         _check(_abi.lib().ftc_protected_conv_launch_ck(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
                                                        _ptr(cd2), arr, n, _stream_ptr(stream)), "launch_ck")
 
+    def launch_cd1(self, D, O, cd1, plan: LayerPlan, faults=(), stream=None):
+        """launch with the clean-path checksum Cd1 = sum_n D_n (FP64, any order) supplied by
+        D's producer, e.g. the start of an ftc_glue_act_pool_cd1 workspace."""
+        arr, n = _faults_c(faults)
+        self._pl = plan.c()
+        _check(_abi.lib().ftc_protected_conv_launch_cd1(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
+                                                        arr, n, _stream_ptr(stream)), "launch_cd1")
+
     def finish(self) -> LayerReport:
         rep = _abi.Report()
         _check(_abi.lib().ftc_protected_conv_finish(self.h, C.byref(rep)), "finish")

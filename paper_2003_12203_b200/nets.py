@@ -222,15 +222,16 @@ class ProtectedNet:
         self.buf = {}
         for name, (c, h) in self.sh.items():
             self.buf[name] = torch.empty((batch, c, h, h), dtype=torch.float32, device=dev)
-        # glue outputs consumed by a protected conv carry that conv's input checksums,
-        # reduced inside the glue kernel (no separate pass over D)
+        # glue outputs consumed by a protected conv carry that conv's clean-path checksum
+        # Cd1, reduced inside the glue kernel (no separate pass over D): a zero-filled
+        # workspace per glue output whose head is Cd1 (ftc_glue_act_pool_cd1)
         conv_srcs = {op.src for op in net["ops"] if isinstance(op, Conv)}
         self.ck = {}
         for op in net["ops"]:
             if isinstance(op, ActPool) and op.dst in conv_srcs:
-                c, h = self.sh[op.dst]
-                self.ck[op.dst] = (torch.empty((c, h, h), dtype=torch.float64, device=dev),
-                                   torch.empty((c, h, h), dtype=torch.float64, device=dev))
+                c, h = self.sh[op.src]
+                n = _abi.lib().ftc_glue_ws_doubles(batch, c, h, op.k, op.s, op.p)
+                self.ck[op.dst] = torch.zeros((int(n),), dtype=torch.float64, device=dev)
         # an act+pool whose output feeds exactly one conv staged channel-last (TMA im2col)
         # writes that layer's NHWC copy in the same pass
         consumers = {}
@@ -250,28 +251,21 @@ class ProtectedNet:
     def set_input(self, x):
         self.buf["x"].copy_(x if not isinstance(x, np.ndarray) else self.torch.from_numpy(x))
 
-    def _glue(self, op, stream):
+    def _glue(self, op, stream, protected=True):
         L = _abi.lib()
         s = stream.cuda_stream
         if isinstance(op, ActPool):
             c, h = self.sh[op.src]
+            ws = self.ck.get(op.dst)
+            nhwc = None
             if op.dst in self.nhwc_target:
-                Lc, ptr = self.nhwc_target[op.dst]
-                cd1, cd2 = self.ck.get(op.dst, (None, None))
-                _check(L.ftc_glue_act_pool_nhwc(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), ptr,
-                                                self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
-                                                cd1.data_ptr() if cd1 is not None else None,
-                                                cd2.data_ptr() if cd2 is not None else None, s),
-                       "act_pool_nhwc")
+                Lc, nhwc = self.nhwc_target[op.dst]
+            _check(L.ftc_glue_act_pool_cd1(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), nhwc,
+                                           self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
+                                           ws.data_ptr() if (ws is not None and protected) else None, s),
+                   "act_pool_cd1")
+            if nhwc:
                 Lc.input_nhwc_ready(self.buf[op.dst])
-            elif op.dst in self.ck:
-                cd1, cd2 = self.ck[op.dst]
-                _check(L.ftc_glue_act_pool_ck(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(),
-                                              self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
-                                              cd1.data_ptr(), cd2.data_ptr(), s), "act_pool_ck")
-            else:
-                _check(L.ftc_glue_act_pool(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), self.batch,
-                                           c, h, ACT[op.act], op.k, op.s, op.p, None, s), "act_pool")
         elif isinstance(op, AddAct):
             _check(L.ftc_glue_add_act(self.buf[op.a].data_ptr(), self.buf[op.b].data_ptr(),
                                       self.buf[op.dst].data_ptr(), self.buf[op.a].numel(), ACT[op.act], s),
@@ -287,9 +281,8 @@ class ProtectedNet:
             if isinstance(op, Conv):
                 L = self.layers[op.dst]
                 if protected and op.src in self.ck:
-                    cd1, cd2 = self.ck[op.src]
-                    L.launch_ck(self.buf[op.src], self.buf[op.dst], cd1, cd2, self.plans[op.dst],
-                                (faults or {}).get(op.dst, ()), stream)
+                    L.launch_cd1(self.buf[op.src], self.buf[op.dst], self.ck[op.src], self.plans[op.dst],
+                                 (faults or {}).get(op.dst, ()), stream)
                     if sync_each:
                         reps[op.dst] = L.finish()
                 elif protected:
@@ -300,7 +293,7 @@ class ProtectedNet:
                 else:
                     L.conv_forward(self.buf[op.src], self.buf[op.dst], stream)
             else:
-                self._glue(op, stream)
+                self._glue(op, stream, protected)
         return reps
 
     def launch(self, faults=None, stream=None):

@@ -60,18 +60,21 @@ def test_net_per_layer_parity_and_clean_verdicts(name, batch):
     pn.close()
 
 
-def test_glue_fused_checksums_are_exact():
+def test_glue_fused_checksums():
+    """The glue kernels hand each protected conv its clean-path Cd1 (FP64 sum over the
+    batch, any order): within 1e-12 of the exact-order input checksum."""
     torch = _torch()
     net, pn = build("alexnet", 4)
     pn.forward()
     torch.cuda.synchronize()
-    for name, (cd1, cd2) in pn.ck.items():
+    assert pn.ck
+    for name, ws in pn.ck.items():
         D = pn.buf[name].cpu().numpy().astype(np.float64)
         c, h = pn.sh[name]
         d = O.dims(4, c, h, 1, 1)
-        r1, r2, _, _ = O.input_checksums(d, D, np.zeros((1, c, 1, 1)))
-        assert np.array_equal(cd1.cpu().numpy(), r1), name
-        assert np.array_equal(cd2.cpu().numpy(), r2), name
+        r1, _, _, _ = O.input_checksums(d, D, np.zeros((1, c, 1, 1)))
+        cd1 = ws[:c * h * h].cpu().numpy().reshape(r1.shape)
+        assert np.abs(cd1 - r1).max() <= 1e-12 * max(1.0, np.abs(r1).max()), name
     pn.close()
 
 

@@ -112,8 +112,56 @@ print("fused ok")
 
 
 @pytest.mark.gpu
-def test_fused_detect_path_verdict_parity():
-    env = dict(os.environ, FTC_FUSED_DETECT="1")
+@pytest.mark.parametrize("env_flag", ["", "FTC_NO_FUSED"])
+def test_fused_detect_path_verdict_parity(env_flag):
+    """Default (fused in-kernel CoC-D) and the side-stream clean path both give the
+    reference's verdicts on seeded output flips."""
+    env = dict(os.environ)
+    if env_flag:
+        env[env_flag] = "1"
     code = _FUSED_SCRIPT.format(root=ROOT, oracle=os.path.join(ROOT, "oracle"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,C,H,act,k,s,p", [(5, 96, 55, 1, 3, 2, 0), (4, 256, 27, 1, 3, 2, 0), (3, 384, 13, 1, 1, 1, 0),
+                                             (2, 64, 224, 1, 2, 2, 0), (3, 64, 112, 2, 3, 2, 1), (6, 40, 20, 2, 2, 2, 0),
+                                             (17, 32, 56, 0, 1, 1, 0), (2, 3, 227, 0, 1, 1, 0)])
+def test_glue_tile_cd1(N, C, H, act, k, s, p):
+    """ftc_glue_act_pool_cd1: NCHW output bitwise = ftc_glue_act_pool, NHWC output = its
+    channel-last transpose, ws head = sum_n out_n (FP64, any order) -- and identical on a
+    second call (the workspace tickets re-arm)."""
+    import torch
+    from paper_2003_12203_b200 import _abi
+    L = _abi.lib()
+    rng = np.random.default_rng(N * 1000 + H)
+    Ho = (H + 2 * p - k) // s + 1
+    x = torch.from_numpy(rng.standard_normal((N, C, H, H)).astype(np.float32)).cuda()
+    ref = torch.empty((N, C, Ho, Ho), device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.ftc_glue_act_pool(x.data_ptr(), ref.data_ptr(), N, C, H, act, k, s, p, None, st) == 0
+    nws = L.ftc_glue_ws_doubles(N, C, H, k, s, p)
+    assert nws >= C * Ho * Ho
+    ws = torch.zeros((nws,), dtype=torch.float64, device="cuda")
+    for rep in range(2):
+        out = torch.full((N, C, Ho, Ho), float("nan"), device="cuda")
+        nhwc = torch.full((N, Ho, Ho, C), float("nan"), device="cuda") if C % 32 == 0 else None
+        assert L.ftc_glue_act_pool_cd1(x.data_ptr(), out.data_ptr(), nhwc.data_ptr() if nhwc is not None else None,
+                                       N, C, H, act, k, s, p, ws.data_ptr(), st) == 0, _abi.last_error()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        if nhwc is not None:
+            assert torch.equal(nhwc, ref.permute(0, 2, 3, 1))
+        cd1 = ws[:C * Ho * Ho].view(C, Ho, Ho).cpu().numpy()
+        exact = ref.double().sum(0).cpu().numpy()
+        assert np.abs(cd1 - exact).max() <= 1e-12 * max(1.0, np.abs(exact).max())
+        if rep == 0:
+            first = cd1.copy()
+        else:
+            assert np.array_equal(first, cd1)
+    # no workspace: outputs only
+    out = torch.empty_like(ref)
+    assert L.ftc_glue_act_pool_cd1(x.data_ptr(), out.data_ptr(), None, N, C, H, act, k, s, p, None, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
