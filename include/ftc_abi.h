@@ -273,6 +273,11 @@ int ftc_make_default_plan(const ftc_layer_dims* dims, double tau, double alpha, 
 int ftc_profile_layer(ftc_layer* layer, const float* D, double tau, int32_t reps, ftc_profile_result* out,
                       void* stream);
 
+/* Seeded uniform draws exactly as Tensor4<T>::random (tensor.hpp:57-66) and
+ * random_weights (model_io.cpp:176-192): std::mt19937_64(seed) through
+ * std::uniform_real_distribution<double>(lo, hi), n values into out (host memory). */
+int ftc_mt64_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out);
+
 /* Channel-last input staging for the TMA im2col engine (C % 32 == 0 layers): the layer
  * keeps an NHWC copy of its input that every launch refreshes from D.  A producer that
  * already wrote D in NHWC form into that buffer (ftc_glue_act_pool_nhwc) calls

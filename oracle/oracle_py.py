@@ -442,3 +442,62 @@ def ref_corpus_to_jsonl(entries) -> str:
     if n < 0:
         raise RuntimeError("ref_corpus_to_jsonl failed")
     return buf.value.decode()
+
+
+# ----------------------------------------------------------------------------- model files / reports
+STAGE_CODES = {"none": 0, "reload": 1, "coc": 2, "rc": 3, "clc": 4, "fc": 5, "discard": 6, "recompute": 7}  # report.hpp:12-21
+
+
+def ref_parse_model_config(text: str) -> int:
+    """parse_model_config status through the reference: 0 ok, 2 ConfigError, 1 ShapeError."""
+    L = ref()
+    L.ref_parse_model_config.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+    n = C.c_int(0)
+    return L.ref_parse_model_config(text.encode(), C.byref(n))
+
+
+def ref_make_weights(config_text: str, seed: int, path: str) -> int:
+    L = ref()
+    L.ref_make_weights.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p]
+    return L.ref_make_weights(config_text.encode(), C.c_uint64(seed), path.encode())
+
+
+def ref_load_weights(config_text: str, path: str) -> int:
+    L = ref()
+    L.ref_load_weights.argtypes = [C.c_char_p, C.c_char_p]
+    return L.ref_load_weights(config_text.encode(), path.encode())
+
+
+def ref_report_to_json(reports, timings=False, campaign=None) -> str:
+    """report_to_json (serialize.cpp:174-193) of LayerReport-like objects through the
+    reference; campaign = (runs, detected, above, recovered, mismatches, fatals) wraps
+    them as a CampaignReport."""
+    L = ref()
+    n = len(reports)
+    names = (C.c_char_p * max(1, n))(*[r.layer.encode() for r in reports])
+    ints, blocks, stages, tkeys, tvals = [], [], [], [], []
+    for r in reports:
+        ints += [int(r.detected), STAGE_CODES[r.stage], int(r.weights_reloaded), int(r.recomputed),
+                 len(r.corrected_blocks), len(r.stages_attempted), len(r.timings), 0]
+        for b in r.corrected_blocks:
+            blocks += [int(b[0]), int(b[1])]
+        stages += [STAGE_CODES[s] for s in r.stages_attempted]
+        for k in sorted(r.timings):
+            tkeys.append(k.encode())
+            tvals.append(float(r.timings[k]))
+    ia = (C.c_int * max(1, len(ints)))(*ints)
+    ba = (C.c_longlong * max(1, len(blocks)))(*blocks)
+    sa = (C.c_int * max(1, len(stages)))(*stages)
+    ka = (C.c_char_p * max(1, len(tkeys)))(*tkeys)
+    va = (C.c_double * max(1, len(tvals)))(*tvals)
+    camp = (C.c_longlong * 7)(*(list(campaign or (0,) * 6) + [0]))
+    cap = 1 << 22
+    out = C.create_string_buffer(cap)
+    L.ref_report_to_json.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_longlong]
+    L.ref_report_to_json.restype = C.c_longlong
+    k = L.ref_report_to_json(n, names, ia, ba, sa, ka, va, int(bool(timings)), int(campaign is not None), camp, out,
+                             cap)
+    if k < 0:
+        raise RuntimeError("ref_report_to_json failed")
+    return out.raw[:k].decode()

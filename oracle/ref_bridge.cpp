@@ -496,3 +496,90 @@ long long ref_corpus_to_jsonl(int n, const ref_spec* specs, const ref_truth* tru
 
 }  // extern "C"
 
+
+// ---- model configs, FTCN weight files and run reports (model_io.cpp, serialize.cpp)
+#include "ftconv/model.hpp"
+
+extern "C" {
+
+static long long put_text(const std::string& t, char* out, long long cap) {
+  if ((long long)t.size() + 1 > cap) return -1;
+  std::memcpy(out, t.c_str(), t.size() + 1);
+  return (long long)t.size();
+}
+
+// parse_model_config status: 0 ok, 2 ConfigError, 1 ShapeError, 3 IoError, -1 other
+int ref_parse_model_config(const char* text, int* n_layers) {
+  try {
+    const ModelConfig cfg = parse_model_config(text);
+    if (n_layers) *n_layers = (int)cfg.layers.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// random_weights(cfg, seed) written by save_weights to `path`
+int ref_make_weights(const char* config_text, std::uint64_t seed, const char* path) {
+  try {
+    const ModelConfig cfg = parse_model_config(config_text);
+    save_weights(path, cfg, random_weights(cfg, seed));
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// load_weights status for the file at `path` against the config
+int ref_load_weights(const char* config_text, const char* path) {
+  try {
+    const ModelConfig cfg = parse_model_config(config_text);
+    (void)load_weights(path, cfg);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// report_to_json over n layer reports.  Per report k: ints[8k..8k+7] = {detected, stage,
+// weights_reloaded, recomputed, n_blocks, n_stages, n_timings, unused}; blocks, stage
+// codes and timing values are consumed in order from their arrays; timing keys from
+// tkeys.  campaign != 0 wraps them in a CampaignReport with the counters in camp[7]
+// (runs, detected, above_threshold, recovered, mismatches, fatals) -- by_stage is
+// tallied from the entries as run_campaign does.
+long long ref_report_to_json(int n, const char* const* names, const int* ints, const long long* blocks,
+                             const int* stages, const char* const* tkeys, const double* tvals, int timings,
+                             int campaign, const long long* camp, char* out, long long cap) {
+  try {
+    std::vector<LayerReport> reps;
+    long long bo = 0, so = 0, to = 0;
+    for (int k = 0; k < n; ++k) {
+      const int* v = ints + 8 * k;
+      LayerReport r;
+      r.layer = names[k];
+      r.detected = v[0] != 0;
+      r.stage = static_cast<ResolveStage>(v[1]);
+      r.weights_reloaded = v[2] != 0;
+      r.recomputed = v[3] != 0;
+      for (int b = 0; b < v[4]; ++b, bo += 2) r.corrected_blocks.push_back({(std::size_t)blocks[bo], (std::size_t)blocks[bo + 1]});
+      for (int s = 0; s < v[5]; ++s) r.stages_attempted.push_back(static_cast<ResolveStage>(stages[so++]));
+      for (int t = 0; t < v[6]; ++t, ++to) r.timings[tkeys[to]] = tvals[to];
+      reps.push_back(r);
+    }
+    if (!campaign) return put_text(report_to_json(reps, timings != 0), out, cap);
+    CampaignReport c;
+    c.runs = (std::size_t)camp[0];
+    c.detected = (std::size_t)camp[1];
+    c.above_threshold = (std::size_t)camp[2];
+    c.recovered = (std::size_t)camp[3];
+    c.ground_truth_mismatches = (std::size_t)camp[4];
+    c.integrity_fatals = (std::size_t)camp[5];
+    for (const LayerReport& r : reps) ++c.by_stage[to_string(r.stage)];
+    c.entries = reps;
+    return put_text(report_to_json(c, timings != 0), out, cap);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -28,7 +28,7 @@ EXPORTS = (
     "ftc_campaign", "ftc_ground_truth_of", "ftc_spec_faults", "ftc_conv_forward_faulted",
     "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
-    "ftc_protected_conv_launch_cd1",
+    "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform",
 )
 
 
@@ -145,6 +145,7 @@ def lib():
         L.ftc_profile_layer.argtypes = [vp, vp, dbl, i32, C.POINTER(ProfileResult), vp]
         L.ftc_layer_desc.argtypes = [vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
+        L.ftc_mt64_uniform.argtypes = [C.c_uint64, dbl, dbl, C.c_int64, vp]
         L.ftc_glue_ws_doubles.argtypes = [i32] * 6
         L.ftc_glue_ws_doubles.restype = C.c_int64
         L.ftc_glue_act_pool_cd1.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <random>
 #include <vector>
 
 #include "ftc_common.cuh"
@@ -151,6 +152,18 @@ int ftc_profile_layer(ftc_layer* L, const float* D, double tau, int32_t reps, ft
   if (out->rc_t0 <= 0 || out->rc_t1 <= 0 || out->rc_t2 <= 0 || out->clc_t0 <= 0 || out->clc_t1 <= 0 ||
       out->clc_t2 <= 0)
     return fallback();
+  return FTC_OK;
+}
+
+// Tensor4<T>::random (tensor.hpp:57-66) and random_weights (model_io.cpp:176-192):
+// std::mt19937_64(seed) through std::uniform_real_distribution<double>(lo, hi) -- the
+// same standard-library engines the reference uses, so model weights and inputs
+// generated from a seed are the reference's bit for bit.
+int ftc_mt64_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
+  if (n < 0 || (n > 0 && !out)) return FTC_INVALID_ARGUMENT;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
   return FTC_OK;
 }
 

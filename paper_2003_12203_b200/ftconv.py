@@ -258,6 +258,11 @@ class ProtectedConv:
         pl = plan.c()
         st = _abi.lib().ftc_protected_conv(self.h, C.byref(pl), _ptr(D), _ptr(O), arr, n,
                                            C.byref(rep), _stream_ptr(stream))
+        if st == 4:  # FTC_INTEGRITY_ERROR
+            # the reference throws after filling the report (workflow.hpp:325-338); keep it
+            err = IntegrityError(f"ftc_protected_conv: {_abi.last_error()}")
+            err.report = LayerReport.from_c(rep)
+            raise err
         _check(st, "ftc_protected_conv")
         return O, LayerReport.from_c(rep)
 
