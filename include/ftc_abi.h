@@ -273,6 +273,30 @@ int ftc_make_default_plan(const ftc_layer_dims* dims, double tau, double alpha, 
 int ftc_profile_layer(ftc_layer* layer, const float* D, double tau, int32_t reps, ftc_profile_result* out,
                       void* stream);
 
+/* ---------------------------------------------------------------- back-propagation
+ * conv_backward (conv.hpp:150-185) and run_protected_backward (workflow.hpp:340-417).
+ * D (N,C,H,H), W (M,C,R,R), dO (N,M,E,E) device FP32; dW (M,C,R,R), dD (N,C,H,H)
+ * device FP32 outputs.  Gradients accumulate in FP64; the protection checks the FP64
+ * gradients (sum_m dW vs conv_backward(D, 0, sum_m dO).dW, sum_n dD vs
+ * conv_backward(0, W, sum_n dO).dD, values_differ(tau)), recomputes once on a
+ * mismatch and returns FTC_INTEGRITY_ERROR if the recompute fails too; outputs are the
+ * checked gradients rounded to FP32.  groups != 1 or bias -> FTC_CONFIG_ERROR. */
+typedef struct ftc_grad_fault {  /* the reference's post_hook as a substitution */
+  int32_t target;                /* 0 dW, 1 dD */
+  int32_t mode;                  /* 0 set, 1 add */
+  int64_t index;                 /* flat NCHW index */
+  double value;
+} ftc_grad_fault;
+typedef struct ftc_backward_report {  /* BackwardReport (workflow.hpp:343-347) */
+  int32_t dw_detected, dd_detected, recomputed;
+} ftc_backward_report;
+int ftc_conv_backward(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, float* dW,
+                      float* dD, void* stream);
+/* hook faults apply to the first pass only, like the reference's post_hook */
+int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, double tau,
+                           const ftc_grad_fault* hook, int32_t n_hook, float* dW, float* dD,
+                           ftc_backward_report* report, void* stream);
+
 /* Seeded uniform draws exactly as Tensor4<T>::random (tensor.hpp:57-66) and
  * random_weights (model_io.cpp:176-192): std::mt19937_64(seed) through
  * std::uniform_real_distribution<double>(lo, hi), n values into out (host memory). */

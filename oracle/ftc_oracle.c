@@ -1073,3 +1073,118 @@ void or_make_default_plan(int N, int M, int Ch, int H, int R, int E, double tau,
   *rc = or_decide_rc(*t0, *t1, *t2, *p_r, 1.0 - *p_r);
   *clc = 0;
 }
+
+/* ------------------------------------------------------------------ back-propagation
+ * conv_backward (conv.hpp:150-185) at T=double: one pass over (n, m, x, y) ascending,
+ * each upstream gradient value scattered into dW and dD over (k, i, j) ascending;
+ * padded taps skipped.  groups != 1 -> ConfigError; dO must be N x M x E x E. */
+int or_conv_backward_f64(const or_dims* d, const double* D, const double* W, const double* dO, double* dW,
+                         double* dD) {
+  int E;
+  if (d->groups != 1) return OR_CONFIG_ERROR;
+  int st = or_check_dims(d, &E);
+  if (st) return st;
+  const int N = d->N, M = d->M, Ch = d->C, R = d->R, H = d->H, U = d->stride, p = d->pad;
+  memset(dW, 0, sizeof(double) * (size_t)M * Ch * R * R);
+  memset(dD, 0, sizeof(double) * (size_t)N * Ch * H * H);
+  for (int n = 0; n < N; ++n)
+    for (int m = 0; m < M; ++m)
+      for (int x = 0; x < E; ++x)
+        for (int y = 0; y < E; ++y) {
+          const double g = dO[(((size_t)n * M + m) * E + x) * E + y];
+          for (int k = 0; k < Ch; ++k)
+            for (int i = 0; i < R; ++i)
+              for (int j = 0; j < R; ++j) {
+                const long long h = (long long)U * x + i - p, w = (long long)U * y + j - p;
+                if (h < 0 || w < 0 || h >= H || w >= H) continue;
+                dW[(((size_t)m * Ch + k) * R + i) * R + j] += D[(((size_t)n * Ch + k) * H + h) * H + w] * g;
+                dD[(((size_t)n * Ch + k) * H + h) * H + w] += W[(((size_t)m * Ch + k) * R + i) * R + j] * g;
+              }
+        }
+  return OR_OK;
+}
+
+/* run_protected_backward (workflow.hpp:350-417) at T=double.  The post_hook is
+ * restated as a substitution list applied to the first pass only: element `index`
+ * of dW (target 0) or dD (target 1) set to `value` (mode 0) or incremented (mode 1).
+ * Returns OR_INTEGRITY_ERROR when the recompute fails verification. */
+static void bwd_check(const or_dims* d, const double* dW, const double* dD, const double* cdw, const double* cdd,
+                      double tau, int* bad_w, int* bad_d) {
+  const int N = d->N, M = d->M, Ch = d->C, R = d->R, H = d->H;
+  *bad_w = *bad_d = 0;
+  for (int k = 0; k < Ch && !*bad_w; ++k)
+    for (int i = 0; i < R && !*bad_w; ++i)
+      for (int j = 0; j < R; ++j) {
+        double s = 0.0;
+        for (int m = 0; m < M; ++m) s += dW[(((size_t)m * Ch + k) * R + i) * R + j];
+        if (or_values_differ(cdw[((size_t)k * R + i) * R + j], s, tau)) {
+          *bad_w = 1;
+          break;
+        }
+      }
+  for (int k = 0; k < Ch && !*bad_d; ++k)
+    for (int a = 0; a < H && !*bad_d; ++a)
+      for (int b = 0; b < H; ++b) {
+        double s = 0.0;
+        for (int n = 0; n < N; ++n) s += dD[(((size_t)n * Ch + k) * H + a) * H + b];
+        if (or_values_differ(cdd[((size_t)k * H + a) * H + b], s, tau)) {
+          *bad_d = 1;
+          break;
+        }
+      }
+}
+
+int or_protected_backward(const or_dims* d, const double* D, const double* W, const double* dO, double tau,
+                          const or_pre_fault* hook, int n_hook, double* dW, double* dD, int* dw_detected,
+                          int* dd_detected, int* recomputed) {
+  int E;
+  if (d->groups != 1) return OR_CONFIG_ERROR;
+  int st = or_check_dims(d, &E);
+  if (st) return st;
+  const int N = d->N, M = d->M, Ch = d->C, R = d->R, H = d->H;
+  *dw_detected = *dd_detected = *recomputed = 0;
+  /* upstream-gradient block sums (workflow.hpp:358-367) */
+  double* rows = calloc((size_t)N * E * E, sizeof(double));
+  double* cols = calloc((size_t)M * E * E, sizeof(double));
+  for (int n = 0; n < N; ++n)
+    for (int m = 0; m < M; ++m)
+      for (int x = 0; x < E; ++x)
+        for (int y = 0; y < E; ++y) {
+          const double g = dO[(((size_t)n * M + m) * E + x) * E + y];
+          rows[((size_t)n * E + x) * E + y] += g;
+          cols[((size_t)m * E + x) * E + y] += g;
+        }
+  /* cdw = conv_backward(D, w1, rows).dW, cdd = conv_backward(d1, W, cols).dD (:369-374) */
+  or_dims dw = *d, dd = *d;
+  dw.M = 1;
+  dd.N = 1;
+  double* w1 = calloc((size_t)Ch * R * R, sizeof(double));
+  double* d1 = calloc((size_t)Ch * H * H, sizeof(double));
+  double* cdw = malloc(sizeof(double) * (size_t)Ch * R * R);
+  double* cdd = malloc(sizeof(double) * (size_t)Ch * H * H);
+  double* junk_d = malloc(sizeof(double) * (size_t)N * Ch * H * H);
+  double* junk_w = malloc(sizeof(double) * (size_t)M * Ch * R * R);
+  or_conv_backward_f64(&dw, D, w1, rows, cdw, junk_d);
+  or_conv_backward_f64(&dd, d1, W, cols, junk_w, cdd);
+  or_conv_backward_f64(d, D, W, dO, dW, dD);
+  for (int h = 0; h < n_hook; ++h) {
+    double* t = hook[h].target == 0 ? dW : dD;
+    if (hook[h].mode == 0)
+      t[hook[h].index] = hook[h].value;
+    else
+      t[hook[h].index] += hook[h].value;
+  }
+  int bw, bd;
+  bwd_check(d, dW, dD, cdw, cdd, tau, &bw, &bd);
+  *dw_detected = bw;
+  *dd_detected = bd;
+  int ret = OR_OK;
+  if (bw || bd) {
+    or_conv_backward_f64(d, D, W, dO, dW, dD);
+    *recomputed = 1;
+    bwd_check(d, dW, dD, cdw, cdd, tau, &bw, &bd);
+    if (bw || bd) ret = OR_INTEGRITY_ERROR;
+  }
+  free(rows); free(cols); free(w1); free(d1); free(cdw); free(cdd); free(junk_d); free(junk_w);
+  return ret;
+}

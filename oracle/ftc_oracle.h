@@ -129,6 +129,15 @@ int or_isolated_scheme(const or_dims* d, const double* D, const double* W_golden
 /* fault.hpp:82-87 -- u ^= 1u << (bit % 31) on the FP32 word */
 float or_flip_bit_f32(float v, unsigned bit);
 
+/* ---- back-propagation (conv.hpp:150-185, workflow.hpp:340-417), T=double ---- */
+int or_conv_backward_f64(const or_dims* d, const double* D, const double* W, const double* dO, double* dW,
+                         double* dD);
+/* hook: post_hook restated as substitutions on the first pass (target 0 dW, 1 dD;
+ * mode 0 set, 1 add) */
+int or_protected_backward(const or_dims* d, const double* D, const double* W, const double* dO, double tau,
+                          const or_pre_fault* hook, int n_hook, double* dW, double* dD, int* dw_detected,
+                          int* dd_detected, int* recomputed);
+
 /* workflow.hpp:55-112 plan helpers */
 double or_cost_model(int scheme, int N, int M, int Ch, int H, int R, int E, double alpha, double beta);
 int or_decide_rc(double t0, double t1, double t2, double p_r, double p_c);

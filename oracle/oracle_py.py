@@ -501,3 +501,58 @@ def ref_report_to_json(reports, timings=False, campaign=None) -> str:
     if k < 0:
         raise RuntimeError("ref_report_to_json failed")
     return out.raw[:k].decode()
+
+
+# ----------------------------------------------------------------------------- back-propagation
+class _GradHook(C.Structure):
+    _fields_ = [("target", C.c_int), ("index", C.c_longlong), ("mode", C.c_int), ("value", C.c_double)]
+
+
+def _hooks(hooks):
+    """hooks: iterable of (target 'dW'|'dD', flat index, mode 'set'|'add', value)"""
+    hooks = list(hooks or ())
+    arr = (_GradHook * max(1, len(hooks)))(*[_GradHook(0 if t == "dW" else 1, int(i), 0 if m == "set" else 1,
+                                                       float(v)) for t, i, m, v in hooks])
+    return arr, len(hooks)
+
+
+def _bwd_shapes(d: Dims):
+    E = extent(d)
+    return (d.M, d.C, d.R, d.R), (d.N, d.C, d.H, d.H), (d.N, d.M, E, E)
+
+
+def conv_backward(d: Dims, D, W, dO, lib=None):
+    """conv_backward<double> (conv.hpp:150-185): oracle restatement, or the reference
+    itself with lib=ref()."""
+    sw, sd, _ = _bwd_shapes(d)
+    dW, dD = np.empty(sw), np.empty(sd)
+    L = lib or oracle()
+    fn = L.or_conv_backward_f64 if L is oracle() else L.ref_conv_backward
+    fn.argtypes = [C.POINTER(Dims)] + [C.c_void_p] * 5
+    st = fn(C.byref(d), P(_f64(D)), P(_f64(W)), P(_f64(dO)), P(dW), P(dD))
+    return st, dW, dD
+
+
+def protected_backward(d: Dims, D, W, dO, tau, hooks=(), lib=None):
+    """run_protected_backward<double> (workflow.hpp:350-417) -> (status, dW, dD,
+    {dw_detected, dd_detected, recomputed})"""
+    sw, sd, _ = _bwd_shapes(d)
+    dW, dD = np.empty(sw), np.empty(sd)
+    arr, n = _hooks(hooks)
+    L = lib or oracle()
+    if L is oracle():
+        f = (C.c_int * 3)()
+        L.or_protected_backward.argtypes = [C.POINTER(Dims)] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_int,
+                                                                                   C.c_void_p, C.c_void_p,
+                                                                                   C.c_void_p, C.c_void_p,
+                                                                                   C.c_void_p]
+        st = L.or_protected_backward(C.byref(d), P(_f64(D)), P(_f64(W)), P(_f64(dO)), tau, arr, n, P(dW), P(dD),
+                                     C.byref(f, 0), C.byref(f, 4), C.byref(f, 8))
+    else:
+        f = (C.c_int * 3)()
+        L.ref_protected_backward.argtypes = [C.POINTER(Dims)] + [C.c_void_p] * 3 + [C.c_double, C.c_void_p, C.c_int,
+                                                                                    C.c_void_p, C.c_void_p,
+                                                                                    C.c_void_p]
+        st = L.ref_protected_backward(C.byref(d), P(_f64(D)), P(_f64(W)), P(_f64(dO)), tau, arr, n, P(dW), P(dD),
+                                      f)
+    return st, dW, dD, {"dw_detected": bool(f[0]), "dd_detected": bool(f[1]), "recomputed": bool(f[2])}

@@ -583,3 +583,68 @@ long long ref_report_to_json(int n, const char* const* names, const int* ints, c
 }
 
 }  // extern "C"
+
+// ---- back-propagation (conv.hpp:150-185, workflow.hpp:340-417) at T=double
+extern "C" {
+
+struct ref_grad_hook {  // post_hook substitution: target 0 dW / 1 dD, mode 0 set / 1 add
+  int target;
+  long long index;
+  int mode;
+  double value;
+};
+
+int ref_conv_backward(const ref_dims* d, const double* D, const double* W, const double* dO, double* dW,
+                      double* dD) {
+  try {
+    const ConvParams p = params(d);
+    Tensor4<double> tD(d->N, d->C, d->H, d->H), tW(d->M, d->C / d->groups, d->R, d->R);
+    std::memcpy(tD.raw().data(), D, tD.size() * sizeof(double));
+    std::memcpy(tW.raw().data(), W, tW.size() * sizeof(double));
+    const std::size_t E = output_extent(d->H, d->R, p);
+    Tensor4<double> tO(d->N, d->M, E, E);
+    std::memcpy(tO.raw().data(), dO, tO.size() * sizeof(double));
+    auto [gw, gd] = conv_backward(tD, tW, tO, p);
+    std::memcpy(dW, gw.raw().data(), gw.size() * sizeof(double));
+    std::memcpy(dD, gd.raw().data(), gd.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_protected_backward(const ref_dims* d, const double* D, const double* W, const double* dO, double tau,
+                           const ref_grad_hook* hook, int n_hook, double* dW, double* dD, int* flags3) {
+  BackwardReport rep;
+  try {
+    const ConvParams p = params(d);
+    Tensor4<double> tD(d->N, d->C, d->H, d->H), tW(d->M, d->C / d->groups, d->R, d->R);
+    std::memcpy(tD.raw().data(), D, tD.size() * sizeof(double));
+    std::memcpy(tW.raw().data(), W, tW.size() * sizeof(double));
+    const std::size_t E = output_extent(d->H, d->R, p);
+    Tensor4<double> tO(d->N, d->M, E, E);
+    std::memcpy(tO.raw().data(), dO, tO.size() * sizeof(double));
+    std::function<void(Tensor4<double>&, Tensor4<double>&)> fn;
+    if (n_hook > 0)
+      fn = [&](Tensor4<double>& gw, Tensor4<double>& gd) {
+        for (int h = 0; h < n_hook; ++h) {
+          double& v = (hook[h].target == 0 ? gw : gd).raw()[hook[h].index];
+          v = hook[h].mode == 0 ? hook[h].value : v + hook[h].value;
+        }
+      };
+    auto [gw, gd] = run_protected_backward(tD, tW, tO, p, tau, rep, fn);
+    std::memcpy(dW, gw.raw().data(), gw.size() * sizeof(double));
+    std::memcpy(dD, gd.raw().data(), gd.size() * sizeof(double));
+    flags3[0] = rep.dw_detected;
+    flags3[1] = rep.dd_detected;
+    flags3[2] = rep.recomputed;
+    return 0;
+  } catch (const std::exception& e) {
+    flags3[0] = rep.dw_detected;
+    flags3[1] = rep.dd_detected;
+    flags3[2] = rep.recomputed;
+    return code_of(e);
+  }
+}
+
+}  // extern "C"

@@ -7,6 +7,7 @@ hand-written sm_100a CUDA kernels behind the C ABI in include/ftc_abi.h
 reference's C++ API (proj/core/include/ftconv/) used by tests and bench.py.
 """
 from .ftconv import (  # noqa: F401
+    BackwardReport, GradFault, conv_backward, run_protected_backward,
     ConfigError, ConvParams, Fault, IntegrityError, IoError, LayerPlan, LayerReport,
     ProtectedConv, ShapeError, conv_forward, detect_coc_d, input_checksums, output_bitflip,
     output_checksums, output_extent, output_summations, run_protected_layer, set_conv_engine,
@@ -14,6 +15,7 @@ from .ftconv import (  # noqa: F401
 )
 
 __all__ = [
+    "BackwardReport", "GradFault", "conv_backward", "run_protected_backward",
     "ConfigError", "ConvParams", "Fault", "IntegrityError", "IoError", "LayerPlan", "LayerReport",
     "ProtectedConv", "ShapeError", "conv_forward", "detect_coc_d", "input_checksums",
     "output_bitflip", "output_checksums", "output_extent", "output_summations",

@@ -28,13 +28,21 @@ EXPORTS = (
     "ftc_campaign", "ftc_ground_truth_of", "ftc_spec_faults", "ftc_conv_forward_faulted",
     "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
-    "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform",
+    "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
 )
 
 
 class ConvDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("N", "C", "H", "M", "R", "stride", "pad", "groups",
                                          "bias_enabled")]
+
+
+class GradFault(C.Structure):
+    _fields_ = [("target", C.c_int32), ("mode", C.c_int32), ("index", C.c_int64), ("value", C.c_double)]
+
+
+class BackwardReport(C.Structure):
+    _fields_ = [("dw_detected", C.c_int32), ("dd_detected", C.c_int32), ("recomputed", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -146,6 +154,9 @@ def lib():
         L.ftc_layer_desc.argtypes = [vp, vp]
         L.ftc_glue_add_act.argtypes = [vp, vp, vp, C.c_int64, i32, vp]
         L.ftc_mt64_uniform.argtypes = [C.c_uint64, dbl, dbl, C.c_int64, vp]
+        L.ftc_conv_backward.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp, vp, vp]
+        L.ftc_protected_backward.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, dbl, C.POINTER(GradFault), i32, vp,
+                                             vp, C.POINTER(BackwardReport), vp]
         L.ftc_glue_ws_doubles.argtypes = [i32] * 6
         L.ftc_glue_ws_doubles.restype = C.c_int64
         L.ftc_glue_act_pool_cd1.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]

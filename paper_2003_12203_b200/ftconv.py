@@ -338,6 +338,70 @@ def conv_forward(D, W, bias, p: ConvParams):
         layer.close()
 
 
+@dataclass
+class BackwardReport:
+    """workflow.hpp:343-347"""
+    dw_detected: bool = False
+    dd_detected: bool = False
+    recomputed: bool = False
+
+
+@dataclass
+class GradFault:
+    """The reference's post_hook (workflow.hpp:350-353) as a substitution on the first
+    pass: dW or dD element `index` (flat NCHW) set to / incremented by `value`."""
+    target: str = "dW"  # "dW" | "dD"
+    index: int = 0
+    mode: str = "add"   # "set" | "add"
+    value: float = 0.0
+
+    def c(self) -> _abi.GradFault:
+        return _abi.GradFault(0 if self.target == "dW" else 1, 0 if self.mode == "set" else 1, int(self.index),
+                              float(self.value))
+
+
+def _bwd_setup(D, W, dO, p: ConvParams):
+    torch = _torch()
+    Dd, Wd, gd = _to_dev(D), _to_dev(W), _to_dev(dO)
+    N, Cin, H = Dd.shape[0], Dd.shape[1], Dd.shape[2]
+    M, R = Wd.shape[0], Wd.shape[2]
+    d = desc(N, Cin, H, M, R, ConvParams(stride=p.stride, pad=p.pad, groups=p.groups, bias_enabled=False))
+    if p.groups != 1:
+        raise ConfigError("grouped back-propagation is unsupported")
+    E = output_extent(H, R, p)
+    if tuple(gd.shape) != (N, M, E, E) or Wd.shape[1] != Cin or Wd.shape[3] != R or Dd.shape[3] != H:
+        raise ShapeError("upstream gradient shape must be N x M x E x E")
+    dW = torch.empty((M, Cin, R, R), dtype=torch.float32, device=Dd.device)
+    dD = torch.empty((N, Cin, H, H), dtype=torch.float32, device=Dd.device)
+    return d, Dd, Wd, gd, dW, dD
+
+
+def conv_backward(D, W, dO, p: ConvParams, stream=None):
+    """conv_backward (conv.hpp:150-185) -> (dW, dD) on the device (FP64 accumulation)."""
+    d, Dd, Wd, gd, dW, dD = _bwd_setup(D, W, dO, p)
+    _check(_abi.lib().ftc_conv_backward(C.byref(d), _ptr(Dd), _ptr(Wd), _ptr(gd), _ptr(dW), _ptr(dD),
+                                        _stream_ptr(stream)), "conv_backward")
+    return dW, dD
+
+
+def run_protected_backward(D, W, dO, p: ConvParams, tau: float, faults=(), stream=None):
+    """run_protected_backward (workflow.hpp:350-417) -> (dW, dD, BackwardReport);
+    IntegrityError (with .report) when the recompute fails verification."""
+    d, Dd, Wd, gd, dW, dD = _bwd_setup(D, W, dO, p)
+    faults = list(faults or ())
+    arr = (_abi.GradFault * max(1, len(faults)))(*[f.c() for f in faults])
+    rep = _abi.BackwardReport()
+    st = _abi.lib().ftc_protected_backward(C.byref(d), _ptr(Dd), _ptr(Wd), _ptr(gd), float(tau), arr, len(faults),
+                                           _ptr(dW), _ptr(dD), C.byref(rep), _stream_ptr(stream))
+    out = BackwardReport(bool(rep.dw_detected), bool(rep.dd_detected), bool(rep.recomputed))
+    if st == 4:  # FTC_INTEGRITY_ERROR
+        err = IntegrityError(f"run_protected_backward: {_abi.last_error()}")
+        err.report = out
+        raise err
+    _check(st, "run_protected_backward")
+    return dW, dD, out
+
+
 def run_protected_layer(D, W, bias, p: ConvParams, plan: LayerPlan, faults=()):
     """workflow.hpp:141-339 -> (O, LayerReport)."""
     Dd = _to_dev(D)
