@@ -341,19 +341,25 @@ class ProtectedNet:
 
 
 class HostPipeline:
-    """Host-buffer inference over a ProtectedNet with the copies overlapped.
+    """Host-buffer inference over ProtectedNets with the copies and the host overlapped.
 
     Each batch is copied in from (pinned) host memory and its result copied back, as
-    with a serial ``set_input -> forward -> output`` loop, but batch k+1's H2D runs on a
-    copy stream under batch k's protected forward (two device input slots), and batch
-    k's result leaves through a device staging copy and an async D2H on a second copy
-    stream.  Verdicts are read per batch (``ProtectedNet.finish``) before the next batch
-    is launched, so repairs and replays behave exactly as in ``forward``."""
+    with a serial ``set_input -> forward -> output`` loop.  With one net, batch k+1's
+    H2D runs on a copy stream under batch k's protected forward (two device input
+    slots) and verdicts are read before the next batch is launched.  With two nets (two
+    complete sets of layer handles and activations, the same weights) batch k+1 is
+    also *launched* before batch k's verdicts are read, so the compute stream never
+    waits for the host; a repair of batch k (``ProtectedNet.finish``) touches only its
+    own net, and its result is staged after it.  Results leave through a device staging
+    copy and an async D2H on a second copy stream."""
 
-    def __init__(self, pn: ProtectedNet):
+    def __init__(self, pns):
+        pns = list(pns) if isinstance(pns, (list, tuple)) else [pns]
+        pn = pns[0]
         torch = pn.torch
-        self.pn, self.torch = pn, torch
-        self.slots = [pn.buf["x"], torch.empty_like(pn.buf["x"])]
+        self.pns, self.torch = pns, torch
+        self.two = len(pns) == 2
+        self.slots = [p.buf["x"] for p in pns] if self.two else [pn.buf["x"], torch.empty_like(pn.buf["x"])]
         out = pn.output()
         self.stage = [torch.empty_like(out), torch.empty_like(out)]
         self.s_in = torch.cuda.Stream(device=out.device)
@@ -363,7 +369,7 @@ class HostPipeline:
         """xs_host[k] -> outs_host[k] for every k; returns the per-batch verdict dicts.
         ``before_step`` is called on the compute stream ahead of each batch (bench.py's L2
         flush); ``start_event`` (recorded on the compute stream) gates the first H2D."""
-        torch, pn = self.torch, self.pn
+        torch = self.torch
         main = torch.cuda.current_stream()
         Ev = torch.cuda.Event
         ev_in, ev_used, ev_staged, ev_out = [Ev(), Ev()], [None, None], [Ev(), Ev()], [None, None]
@@ -378,23 +384,33 @@ class HostPipeline:
                 self.slots[s].copy_(xs_host[k], non_blocking=True)
             ev_in[s].record(self.s_in)
 
-        reps = []
-        K = len(xs_host)
-        if K:
-            h2d(0)
-        for k in range(K):
+        def net_of(k):
+            return self.pns[k % 2] if self.two else self.pns[0]
+
+        ev_launched = [Ev(), Ev()]
+
+        def launch(k):
             s = k % 2
-            if k + 1 < K:
-                h2d(k + 1)
             main.wait_event(ev_in[s])
             if before_step is not None:
                 before_step()
+            pn = net_of(k)
             pn.buf["x"] = self.slots[s]
             pn.launch(faults, main)
-            reps.append(pn.finish(main))
-            used = Ev()
-            used.record(main)
-            ev_used[s] = used
+            ev_launched[s].record(main)
+
+        def drain(k):
+            s = k % 2
+            pn = net_of(k)
+            rep = pn.finish(main)
+            if self.two and not any(r.detected for r in rep.values()):
+                # clean: the input slot is free once batch k's kernels ran (not after
+                # batch k+1's, which were enqueued before this finish)
+                ev_used[s] = ev_launched[s]
+            else:
+                used = Ev()
+                used.record(main)
+                ev_used[s] = used
             if ev_out[s] is not None:  # the D2H two batches back has drained this stage
                 main.wait_event(ev_out[s])
             self.stage[s].copy_(pn.output(), non_blocking=True)
@@ -405,10 +421,29 @@ class HostPipeline:
             done = Ev()
             done.record(self.s_out)
             ev_out[s] = done
+            return rep
+
+        reps = []
+        K = len(xs_host)
+        if K:
+            h2d(0)
+            if self.two:
+                launch(0)
+        for k in range(K):
+            if k + 1 < K:
+                h2d(k + 1)
+                if self.two:
+                    launch(k + 1)  # enqueued before batch k's verdicts are read
+            if not self.two:
+                launch(k)
+            reps.append(drain(k))
         for e in ev_out:
             if e is not None:
                 main.wait_event(e)
-        pn.buf["x"] = self.slots[0]
+        for pn, x in zip(self.pns, self.slots):
+            pn.buf["x"] = x
+        if not self.two:
+            self.pns[0].buf["x"] = self.slots[0]
         return reps
 
 
@@ -479,7 +514,10 @@ class BenchNet:
     def e2e_stream(self, steps, before_step=None, start_event=None):
         """`steps` host batches through HostPipeline (H2D/D2H overlapped with compute)."""
         if not hasattr(self, "pipe"):
-            self.pipe = HostPipeline(self.pn)
+            # a second set of layer handles and activations (same weights and plans) so
+            # batch k+1 is enqueued while batch k's verdicts are read
+            self.pn2 = ProtectedNet(self.net, self.batch, 11, self.pn.dev, self.taus)
+            self.pipe = HostPipeline([self.pn, self.pn2])
             self.outs_host = [self.out_host, self.pn.torch.empty_like(self.out_host).pin_memory()]
         reps = self.pipe.run([self.x_host] * steps, [self.outs_host[k % 2] for k in range(steps)],
                              before_step, start_event)

@@ -141,9 +141,11 @@ def test_net_layer_verdict_matches_oracle():
     pn.close()
 
 
-def test_host_pipeline_matches_serial_forward():
-    """HostPipeline (H2D of batch k+1 under batch k, staged D2H) returns, per batch,
-    bitwise the output and the verdicts of a serial set_input -> forward -> output."""
+@pytest.mark.parametrize("depth", [1, 2])
+def test_host_pipeline_matches_serial_forward(depth):
+    """HostPipeline (H2D of batch k+1 under batch k, staged D2H; with two nets batch k+1
+    is also launched before batch k's verdicts are read) returns, per batch, bitwise the
+    output and the verdicts of a serial set_input -> forward -> output."""
     import paper_2003_12203_b200 as F
     torch = _torch()
     net, pn = build("alexnet", 2)
@@ -153,7 +155,8 @@ def test_host_pipeline_matches_serial_forward():
         pn.set_input(x.cuda())
         reps = pn.forward()
         want.append((pn.output().cpu().clone(), {k: r.stage for k, r in reps.items()}))
-    pipe = nets.HostPipeline(pn)
+    pn2 = nets.ProtectedNet(net, 2, 11, torch.device("cuda")) if depth == 2 else None
+    pipe = nets.HostPipeline([pn, pn2] if pn2 else pn)
     outs = [torch.empty(pn.output().shape).pin_memory() for _ in xs]
     got = pipe.run(xs, outs)
     torch.cuda.synchronize()
@@ -168,3 +171,5 @@ def test_host_pipeline_matches_serial_forward():
         assert got[k]["c3"].detected
         assert torch.equal(outs[k], want[k][0]), k
     pn.close()
+    if pn2:
+        pn2.close()
