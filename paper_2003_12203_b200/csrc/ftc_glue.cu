@@ -20,87 +20,20 @@ __device__ __forceinline__ float act_fn(float v, int act) {
   return v;
 }
 
-// out[n,c,ox,oy] = max over the k x k window (stride s, padding p, -inf padding)
-// of act(in[n,c,.,.]); k = 1, s = 1 is a plain activation.  Grid: y = (n, c) plane
-// (strided when N*C exceeds the grid limit), x = output positions of the plane; 32-bit
-// index math (a 64-bit div/mod per element made this kernel integer-bound).
+// act + pool, NCHW output only, one thread per output element (flat over (n, c, x, y)
+// with 32-bit index math): no idle threads on small planes (a plane-per-block-row grid
+// left 86% of the threads of a 6x6-output pool idle).
 template <int KT>
-__global__ void __launch_bounds__(256) k_act_pool(const float* __restrict__ in, float* __restrict__ out,
-                                                 int NC, int H, int act, int kr, int s, int p, int Ho) {
-  constexpr int kPlanes = 4;  // planes per thread: their window loads are all in flight
+__global__ void __launch_bounds__(256) k_act_pool_flat(const float* __restrict__ in, float* __restrict__ out,
+                                                      unsigned total, int H, int Ho, int act, int kr, int s, int p) {
   const int k = KT > 0 ? KT : kr;
-  const int plane = Ho * Ho;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= plane) return;
-  const int ox = idx / Ho, oy = idx - (idx / Ho) * Ho;
-  const int x0 = ox * s - p, y0 = oy * s - p;
-  for (int nc0 = blockIdx.y * kPlanes; nc0 < NC; nc0 += gridDim.y * kPlanes) {
-    if constexpr (KT > 0) {
-      float v[kPlanes][KT * KT];
-#pragma unroll
-      for (int u = 0; u < kPlanes; ++u) {
-        const float* src = in + (long long)(nc0 + u) * H * H;
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-#pragma unroll
-          for (int j = 0; j < KT; ++j) {
-            const int x = x0 + i, y = y0 + j;
-            const bool ok = nc0 + u < NC && x >= 0 && x < H && y >= 0 && y < H;
-            v[u][i * KT + j] = ok ? __ldg(src + x * H + y) : -INFINITY;
-          }
-      }
-#pragma unroll
-      for (int u = 0; u < kPlanes; ++u) {
-        if (nc0 + u >= NC) break;
-        float m = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-#pragma unroll
-          for (int j = 0; j < KT; ++j) {
-            const int x = x0 + i, y = y0 + j;
-            // padding positions are skipped (not act(-inf)) exactly as the generic path
-            if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[u][i * KT + j], act));
-          }
-        out[(long long)(nc0 + u) * plane + idx] = m;
-      }
-    } else {
-      for (int u = 0; u < kPlanes && nc0 + u < NC; ++u) {
-        const float* src = in + (long long)(nc0 + u) * H * H;
-        float m = -INFINITY;
-        for (int i = 0; i < k; ++i) {
-          const int x = x0 + i;
-          if (x < 0 || x >= H) continue;
-          for (int j = 0; j < k; ++j) {
-            const int y = y0 + j;
-            if (y < 0 || y >= H) continue;
-            m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
-          }
-        }
-        out[(long long)(nc0 + u) * plane + idx] = m;
-      }
-    }
-  }
-}
-
-// act + pool of one image's 32-channel x 8-position tile, written NCHW and, through
-// shared memory, NHWC (the next conv's TMA im2col input): loads by channel rows of 8
-// consecutive positions, stores by position rows of 32 channels (128 bytes)
-template <int KT>
-__global__ void __launch_bounds__(256) k_act_pool_t(const float* __restrict__ in, float* __restrict__ out,
-                                                   float* __restrict__ out_t, int C, int H, int act, int kr, int s,
-                                                   int p, int Ho) {
-  __shared__ float tile[8][33];
-  const int k = KT > 0 ? KT : kr;
-  const int plane = Ho * Ho;
-  const int tid = threadIdx.x;
-  const int cl = tid >> 3, pl = tid & 7;
-  const int c = blockIdx.y * 32 + cl, pos = blockIdx.x * 8 + pl;
-  const long long n = blockIdx.z;
-  float m = -INFINITY;
-  if (pos < plane) {
-    const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
+  const unsigned plane = (unsigned)(Ho * Ho);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const unsigned pl = e / plane, pos = e - pl * plane;
+    const int ox = (int)(pos / (unsigned)Ho), oy = (int)pos - ox * Ho;
     const int x0 = ox * s - p, y0 = oy * s - p;
-    const float* src = in + (n * C + c) * H * H;
+    const float* src = in + (long long)pl * H * H;
+    float m = -INFINITY;
     if constexpr (KT > 0) {
       float v[KT * KT];
 #pragma unroll
@@ -108,40 +41,24 @@ __global__ void __launch_bounds__(256) k_act_pool_t(const float* __restrict__ in
 #pragma unroll
         for (int j = 0; j < KT; ++j) {
           const int x = x0 + i, y = y0 + j;
-          v[i * KT + j] = (x >= 0 && x < H && y >= 0 && y < H) ? __ldg(src + x * H + y) : 0.f;
+          v[i * KT + j] = ((unsigned)x < (unsigned)H && (unsigned)y < (unsigned)H) ? __ldg(src + x * H + y) : 0.f;
         }
 #pragma unroll
       for (int i = 0; i < KT; ++i)
 #pragma unroll
-        for (int j = 0; j < KT; ++j) {
-          const int x = x0 + i, y = y0 + j;
-          if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[i * KT + j], act));
-        }
+        for (int j = 0; j < KT; ++j)
+          if ((unsigned)(x0 + i) < (unsigned)H && (unsigned)(y0 + j) < (unsigned)H)
+            m = fmaxf(m, act_fn(v[i * KT + j], act));
     } else {
-      for (int i = 0; i < k; ++i) {
-        const int x = x0 + i;
-        if (x < 0 || x >= H) continue;
-        for (int j = 0; j < k; ++j) {
-          const int y = y0 + j;
-          if (y < 0 || y >= H) continue;
-          m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
-        }
-      }
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j)
+          if ((unsigned)(x0 + i) < (unsigned)H && (unsigned)(y0 + j) < (unsigned)H)
+            m = fmaxf(m, act_fn(__ldg(src + (x0 + i) * H + y0 + j), act));
     }
-    out[(n * C + c) * plane + pos] = m;
+    out[e] = m;
   }
-  tile[pl][cl] = m;
-  __syncthreads();
-  const int wc = tid & 31, wp = tid >> 5;
-  const int spos = blockIdx.x * 8 + wp;
-  if (spos < plane) out_t[(n * plane + spos) * C + blockIdx.y * 32 + wc] = tile[wp][wc];
 }
 
-// Clean-path Cd1 = sum_n D_n (FP64, any order -- CoC-D is tolerance based; the error
-// path recomputes the exact-order checksums, checksums.hpp:100-107).  Workspace
-// [Cd1][G partial slabs][tickets], zero-filled once: block (x, g) sums image group g at
-// 256 positions (one per thread, 8 loads in flight), and the last group block of each x
-// folds the slabs into Cd1 (g ascending) and re-arms its ticket.
 // Workspace layout shared by the Cd1 producers (Cd1Ws): [Cd1: per][tickets][G slabs]
 struct Cd1Ws {
   long long per;       // C * H * H
@@ -166,6 +83,11 @@ __device__ __forceinline__ bool ws_arrive(double* ws, long long tick_off, int ti
   return s_last != 0;
 }
 
+// Clean-path Cd1 = sum_n D_n (FP64, any order -- CoC-D is tolerance based; the error
+// path recomputes the exact-order checksums, checksums.hpp:100-107).  Workspace
+// [Cd1][G partial slabs][tickets], zero-filled once: block (x, g) sums image group g at
+// 256 positions (one per thread, 8 loads in flight), and the last group block of each x
+// folds the slabs into Cd1 (g ascending) and re-arms its ticket.
 __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, int N, long long per, int NG,
                                                   double* __restrict__ ws, long long tick_off, long long slab_off) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -274,18 +196,95 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
   }
 }
 
+// act + pool of a 32-position x 32-channel tile of one image per block (no checksum):
+// warp w pools channels w, w+8, w+16, w+24 at the tile's 32 positions (lane = position:
+// coalesced NCHW rows), and the tile goes channel-last through shared memory (128-byte
+// NHWC rows).  AlexNet pool1 74 us vs 86 us with 8-position tiles.
+template <int KT>
+__global__ void __launch_bounds__(256) k_act_pool_tile(const float* __restrict__ in, float* __restrict__ out,
+                                                      float* __restrict__ out_t, int C, int H, int act, int kr, int s,
+                                                      int p, int Ho) {
+  __shared__ float tile[32][33];
+  const int k = KT > 0 ? KT : kr;
+  const int plane = Ho * Ho;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pos = blockIdx.x * 32 + lane;
+  const bool ok = pos < plane;
+  const int c0 = blockIdx.y * 32;
+  const int n = blockIdx.z;
+  int x0 = 0, y0 = 0;
+  uint32_t rmask = 0, cmask = 0;
+  if (ok) {
+    const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
+    x0 = ox * s - p;
+    y0 = oy * s - p;
+    for (int i = 0; i < k && i < 32; ++i) {
+      if ((unsigned)(x0 + i) < (unsigned)H) rmask |= 1u << i;
+      if ((unsigned)(y0 + i) < (unsigned)H) cmask |= 1u << i;
+    }
+  }
+  const long long HH = (long long)H * H;
+  {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cl = warp + 8 * q, c = c0 + cl;
+      float m = -INFINITY;
+      if (ok && c < C) {
+        const float* src = in + ((long long)n * C + c) * HH + (long long)x0 * H + y0;
+        if constexpr (KT > 0) {
+          float v[KT * KT];
+#pragma unroll
+          for (int i = 0; i < KT; ++i)
+#pragma unroll
+            for (int j = 0; j < KT; ++j)
+              v[i * KT + j] = ((rmask >> i) & (cmask >> j) & 1u) ? __ldg(src + i * H + j) : 0.f;
+#pragma unroll
+          for (int i = 0; i < KT; ++i)
+#pragma unroll
+            for (int j = 0; j < KT; ++j)
+              if ((rmask >> i) & (cmask >> j) & 1u) m = fmaxf(m, act_fn(v[i * KT + j], act));
+        } else {
+          for (int i = 0; i < k; ++i)
+            for (int j = 0; j < k; ++j)
+              if ((rmask >> i) & (cmask >> j) & 1u) m = fmaxf(m, act_fn(__ldg(src + i * H + j), act));
+        }
+        out[((long long)n * C + c) * plane + pos] = m;
+      }
+      tile[lane][cl] = m;
+    }
+    if (out_t) {
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pl = warp + 8 * q, sp = blockIdx.x * 32 + pl;
+        if (sp < plane && c0 + lane < C) out_t[((long long)n * plane + sp) * C + c0 + lane] = tile[pl][lane];
+      }
+    }
+  }
+}
+
 int launch_act_pool(const float* in, float* out, int NC, int H, int act, int k, int s, int p, int Ho,
                     cudaStream_t st) {
-  const int gy = (NC + 3) / 4;
-  const dim3 g((unsigned)((Ho * Ho + 255) / 256), (unsigned)(gy < 65535 ? gy : 65535));
-  if (k == 3)
-    FTC_LAUNCH(k_act_pool<3><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
-  else if (k == 2)
-    FTC_LAUNCH(k_act_pool<2><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
-  else if (k == 1)
-    FTC_LAUNCH(k_act_pool<1><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
-  else
-    FTC_LAUNCH(k_act_pool<0><<<g, 256, 0, st>>>(in, out, NC, H, act, k, s, p, Ho));
+  const long long total = (long long)NC * Ho * Ho;
+  // 32-bit flat index per launch; larger tensors go in plane chunks
+  const long long plane = (long long)Ho * Ho, chunk_planes = ((1LL << 31) / plane);
+  for (long long p0 = 0; p0 < NC; p0 += chunk_planes) {
+    const long long np = (NC - p0) < chunk_planes ? (NC - p0) : chunk_planes;
+    const unsigned tot = (unsigned)(np * plane);
+    long long blocks = ((long long)tot + 255) / 256;
+    if (blocks > 148LL * 64) blocks = 148LL * 64;
+    const float* ip = in + p0 * H * H;
+    float* op = out + p0 * plane;
+#define FTC_APF(KT) FTC_LAUNCH(k_act_pool_flat<KT><<<(unsigned)blocks, 256, 0, st>>>(ip, op, tot, H, Ho, act, k, s, p))
+    switch (k) {
+      case 1: FTC_APF(1); break;
+      case 2: FTC_APF(2); break;
+      case 3: FTC_APF(3); break;
+      default: FTC_APF(0); break;
+    }
+#undef FTC_APF
+  }
+  (void)total;
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -368,15 +367,16 @@ long long cd1_ws_doubles(int N, long long per) { return cd1_ws_doubles_g(N, 0, 0
 int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k, int s,
                          int p, cudaStream_t st) {
   const int Ho = (H + 2 * p - k) / s + 1;
-  const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)N);
-  if (k == 3)
-    FTC_LAUNCH(k_act_pool_t<3><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
-  else if (k == 2)
-    FTC_LAUNCH(k_act_pool_t<2><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
-  else if (k == 1)
-    FTC_LAUNCH(k_act_pool_t<1><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
-  else
-    FTC_LAUNCH(k_act_pool_t<0><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho));
+  const dim3 g((unsigned)((Ho * Ho + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
+#define FTC_APT(KT) \
+  FTC_LAUNCH(k_act_pool_tile<KT><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho))
+  switch (k) {
+    case 1: FTC_APT(1); break;
+    case 2: FTC_APT(2); break;
+    case 3: FTC_APT(3); break;
+    default: FTC_APT(0); break;
+  }
+#undef FTC_APT
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -393,6 +393,9 @@ int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStrea
 
 int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k,
                              int s, int p, double* ws, cudaStream_t st) {
+  // 8-position x 32-channel tiles looping over image groups: measured faster for the
+  // Cd1-producing pass than 32 x 32 tiles (fewer, longer-running blocks were latency
+  // bound: AlexNet pool2 59 vs 74 us)
   const int Ho = (H + 2 * p - k) / s + 1;
   const long long per = (long long)C * Ho * Ho;
   const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
