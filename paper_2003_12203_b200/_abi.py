@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libftconv_b200.so")
+LIB_PATH = os.environ.get("FTC_LIB_PATH") or os.path.join(PKG, "libftconv_b200.so")  # override: experiments only
 
 MAX_BLOCKS = 4096
 MAX_STAGES = 8

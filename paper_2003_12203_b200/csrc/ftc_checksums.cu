@@ -475,6 +475,80 @@ __global__ void __launch_bounds__(256) k_detect_fused(const double* __restrict__
   }
 }
 
+// Fused clean path, small layers: Co5 (as k_co5_adapt) and CoC-D against the So5 the
+// conv accumulated, in one launch after the conv -- Co5 need not exist before it.
+template <int RT>
+__global__ void __launch_bounds__(256) k_co5_detect(const double* __restrict__ cd1, const double* __restrict__ cw1,
+                                                   double* __restrict__ co5, double* __restrict__ so5, int N, int C,
+                                                   int H, int Rrt, int U, int pad, int E, int P, int bias,
+                                                   const double* agg, double tau, DetectStats* st,
+                                                   unsigned int* ticket, DetectStats* host_out) {
+  __shared__ double red[256];
+  const int R = RT > 0 ? RT : Rrt, RR = R * R, E2 = E * E, S = 256 / P;
+  const int t = threadIdx.x, pl = t % P, sl = t / P;
+  const int f = blockIdx.x * P + pl;
+  double c5 = 0.0;
+  if (f < E2) {
+    const int x = f / E, y = f - (f / E) * E;
+    const int hb = x * U - pad, wb = y * U - pad;
+    for (int c = sl; c < C; c += S) {
+      const double* src = cd1 + (long long)c * H * H;
+      const double* ker = cw1 + c * RR;
+      for (int i = 0; i < R; ++i) {
+        const int hh = hb + i;
+        if (hh < 0 || hh >= H) continue;
+        for (int j = 0; j < R; ++j) {
+          const int ww = wb + j;
+          if (ww < 0 || ww >= H) continue;
+          c5 = fma(__ldg(src + hh * H + ww), __ldg(ker + i * R + j), c5);
+        }
+      }
+    }
+  }
+  red[t] = c5;
+  __syncthreads();
+  int bad = 0;
+  unsigned long long devb = 0ull;
+  if (t < P && f < E2) {
+    double c = 0.0;
+    for (int q = 0; q < S; ++q) c += red[q * P + t];
+    co5[f] = c;
+    double ss = __ldcg(so5 + f);
+    so5[f] = 0.0;
+    if (bias) ss -= (double)N * agg[0];
+    double den = fabs(c);
+    if (den < fabs(ss)) den = fabs(ss);
+    if (den < 1.0) den = 1.0;
+    const double dev = fabs(c - ss) / den;
+    if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
+    bad = values_differ(c, ss, tau) ? 1 : 0;
+  }
+  if (t < 32) {  // P <= 32: the compares live in warp 0
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+      devb = other > devb ? other : devb;
+    }
+    if (t == 0) {
+      if (bad) atomicAdd(&st->flagged, bad);
+      if (devb) atomicMax(&st->max_rel_dev_bits, devb);
+      __threadfence();
+      const unsigned int done = atomicAdd(ticket, 1u);
+      if (done == gridDim.x - 1) {
+        __threadfence();
+        const int fl = atomicExch(&st->flagged, 0);
+        const unsigned long long mb = atomicExch(&st->max_rel_dev_bits, 0ull);
+        volatile DetectStats* h = host_out;
+        h->flagged = fl;
+        h->max_rel_dev_bits = mb;
+        __threadfence_system();
+        *ticket = 0u;
+      }
+    }
+  }
+}
+
 inline int pick_positions(int work_per_position) {
   // slices S ~ work/4 (a few serial steps per thread), P = 256 / S positions per block
   int S = 16;
@@ -589,6 +663,24 @@ int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N,
   const int P = pick_positions(N * parts);
   FTC_LAUNCH(k_detect_adapt<<<(E2 + P - 1) / P, 256, 0, s>>>(co5, rowsum, parts, N, E2, bias, agg, tau, st, ticket,
                                                              host_out, P));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double* so5, int N, int C, int H, int R,
+                      int U, int pad, int E, int bias, const double* agg, double tau, DetectStats* st,
+                      unsigned int* ticket, DetectStats* host_out, cudaStream_t s) {
+  // positions per block: as many slices as fill ~2 waves of 256-thread blocks, P <= 32
+  const int E2 = E * E;
+  int P = 32;
+  while (P > 1 && (E2 + P - 1) / P < 2 * 148 * 4 && 256 / P < C) P >>= 1;
+  const int g = (E2 + P - 1) / P;
+  if (R == 3)
+    FTC_LAUNCH(k_co5_detect<3><<<g, 256, 0, s>>>(cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg, tau, st,
+                                                 ticket, host_out));
+  else
+    FTC_LAUNCH(k_co5_detect<0><<<g, 256, 0, s>>>(cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg, tau, st,
+                                                 ticket, host_out));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -210,6 +210,9 @@ int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStrea
 // The act+pool glue kernels write the next layer's Cd1 the same way.
 int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
                         DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s);
+int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double* so5, int N, int C, int H, int R,
+                      int U, int pad, int E, int bias, const double* agg, double tau, DetectStats* st,
+                      unsigned int* ticket, DetectStats* host_out, cudaStream_t s);
 int launch_co5_taps(const double* cw1, int C, int H, int R, Co5Tap* taps, cudaStream_t s);
 long long cd1_ws_doubles(int N, long long per);
 // C, Ho: the pooling producer's shape when the workspace is shared with it (0, 0: none)

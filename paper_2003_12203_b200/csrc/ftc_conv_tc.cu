@@ -51,7 +51,10 @@
 namespace ftc {
 
 struct TcPlan {
+  // grouped convs: groups x ntg N-tiles, tile nt belongs to group nt / ntg and covers its
+  // kernels [nt % ntg * BN, +BN) of Mg; K = Ckw * R * R per group
   int BN = 0, ntiles = 0, nkc = 0, K = 0, M = 0, G = 1;
+  int groups = 1, Mg = 0, ntg = 0, Ckw = 0, Ctot = 0;
   // channel-last gather (C % 32 == 0): the input is transposed to NHWC per launch and
   // K runs tap-major (k = (i*R + j)*C + c), so a K chunk is 32 consecutive channels of
   // one tap: one bounds test and four 16-byte loads per producer thread per chunk
@@ -102,6 +105,7 @@ struct TcArgs {
   const float* bias;
   float* O;
   int N, C, H, M, R, U, pad, E, K, nkc, BN, ntiles;
+  int Ckw, Mg, ntg;  // grouped convs: channels / kernels per group, N-tiles per group
   int G;           // K chunks per accumulator drain
   int SB;          // B (shared-memory) pipeline stages
   int dbg;         // FTC_TC_DEBUG bits (profiling experiments only; 0 in production)
@@ -260,7 +264,7 @@ __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int
 // chunk); 2: TMA im2col into shared memory, producers only split and store to TMEM.
 // FUSE: clean-path CoC-D operands inside the kernel: the checksum warp computes Co5, the
 // epilogue adds its row sums into So5; launch_detect_fused compares them afterwards.
-template <int BN, int MODE, bool FUSE>
+template <int BN, int MODE, bool FUSE, bool GROUPED>
 __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_constant__ CUtensorMap tmA) {
   constexpr bool NHWC = MODE == 1;
   constexpr bool TMAA = MODE >= 2;
@@ -407,8 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           if ((unsigned)(yb + i) < (unsigned)H) okmask |= 1u << (16 + i);
         }
       }
-      const float* base = NHWC ? a.D + (((long long)n * H + xb) * H + yb) * a.C + hf * 16
-                               : a.D + (long long)n * a.C * HH + (long long)xb * H + yb;
+      // grouped convs: the tile's group's first channel (compile-time 0 otherwise -- any
+      // extra live value in this kernel costs the ungrouped hot loops registers)
+      const int cg = GROUPED ? (t / a.npt) / a.ntg * a.Ckw : 0;
+      const float* base = NHWC ? a.D + (((long long)n * H + xb) * H + yb) * a.C + cg + hf * 16
+                               : a.D + ((long long)n * a.C + cg) * HH + (long long)xb * H + yb;
       // software pipeline: the gathers of chunk kc+1 are in flight while chunk kc is
       // split, waited for and stored into TMEM
       auto gather = [&](int kc, float (&out)[16]) {
@@ -475,9 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
     // ================= B loader =================
     if (lane == 0) {
       uint32_t g = 0, sB = 0, phB = 0, sa = 0, pha = 0;
-      const int ncb = a.C / 32;
+      const int ncb = (GROUPED ? a.Ckw : a.C) / 32;
       for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
         const int nt = t / a.npt;
+        const int cg = GROUPED ? nt / a.ntg * a.Ckw : 0;  // the tile's group's first channel
         const float* src = a.Wp + (long long)nt * a.nkc * 2 * BN * kBK;
         // MODE 2: the tile's first output pixel, as a TMA im2col traversal start
         const long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
               mbar_arrive(fullAs0 + 8 * sa);
             } else {
               mbar_arrive_expect_tx(fullAs0 + 8 * sa, kAStageBytes);
-              tma_im2col_4d(as_base + sa * kAStageBytes, &tmA, cb * 32, cw, ch, n0, (uint16_t)tj, (uint16_t)ti,
+              tma_im2col_4d(as_base + sa * kAStageBytes, &tmA, cg + cb * 32, cw, ch, n0, (uint16_t)tj, (uint16_t)ti,
                             fullAs0 + 8 * sa);
             }
             if (++sa == (uint32_t)kAS) { sa = 0; pha ^= 1u; }
@@ -704,8 +712,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       // the values go back into TMEM and a rolled loop with one out-of-line call per
       // column stores them (an unrolled hook body per column is instruction-cache bound).
       double rs = 0.0, rsm = 0.0;
-      const int m0 = nt * BN + half * HALF;
-      const int mlim = min(HALF, a.M - m0);
+      int m0 = nt * BN + half * HALF, mlim = min(HALF, a.M - m0);
+      if constexpr (GROUPED) {
+        const int mg0 = nt / a.ntg * a.Mg;  // the group's first kernel
+        m0 = mg0 + (nt % a.ntg) * BN + half * HALF;
+        mlim = min(HALF, mg0 + a.Mg - m0);
+      }
       float* op = a.O + ((long long)n * a.M + m0) * E2 + f;
       const float* bp = a.bias ? a.bias + m0 : nullptr;
       if (mlim == HALF && !a.nfaults && !a.plane_mask) {
@@ -803,7 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
 
 // W -> [ntiles][nkc][hi,lo][BN][32] with the SW128 chunk swizzle (16-byte chunk
 // index XOR row%8), rows >= M and k >= K zero-padded.
-__global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, int M, int K, int BN,
+__global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, int Mg, int ntg, int K, int BN,
                          int ntiles, int nkc, int C, int RR, int tap_major) {
   const long long total = (long long)ntiles * nkc * BN * kBK;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -812,10 +824,11 @@ __global__ void k_pack_w(const float* __restrict__ W, float* __restrict__ Wp, in
     const int row = (int)((e / kBK) % BN);
     const int kc = (int)((e / ((long long)kBK * BN)) % nkc);
     const int nt = (int)(e / ((long long)kBK * BN * nkc));
-    const int m = nt * BN + row, kk = kc * kBK + k;
+    // tile nt = (group, N-tile within the group); C = channels per group
+    const int ml = (nt % ntg) * BN + row, m = nt / ntg * Mg + ml, kk = kc * kBK + k;
     // tap-major K (NHWC gather): kk = t*C + c  <->  reference index c*RR + t
     const long long src = tap_major ? (long long)m * K + (long long)(kk % C) * RR + kk / C : (long long)m * K + kk;
-    const float w = (m < M && kk < K) ? W[src] : 0.f;
+    const float w = (ml < Mg && kk < K) ? W[src] : 0.f;
     const float hi = tf32_rn(w), lo = tf32_rn(w - hi);
     const long long tile = ((long long)nt * nkc + kc) * 2;
     const int sw = row * kBK + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3);
@@ -902,17 +915,69 @@ __global__ void __launch_bounds__(256) k_nhwc_cd(const float* __restrict__ D, fl
   }
 }
 
+// k_nhwc_cd with 32-channel x 32-position tiles: warp w loads channels w, w+8, w+16,
+// w+24 (lane = position, 128-byte rows) for 4 images at a time (16 loads in flight per
+// thread), accumulates the exact-order checksums of its 4 (c, position) items over n
+// ascending, and writes each image's tile channel-last through shared memory.
+__global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, float* __restrict__ Dt, int C,
+                                                  int HW, int nimg, double* __restrict__ cd1,
+                                                  double* __restrict__ cd2) {
+  __shared__ float t[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hw = blockIdx.x * 32 + lane;
+  const bool ok = hw < HW;
+  const int c0 = blockIdx.y * 32;
+  double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+  for (int n0 = 0; n0 < nimg; n0 += 4) {
+    float v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + warp + 8 * q;
+        v[u][q] = (ok && n0 + u < nimg) ? __ldg(D + ((long long)(n0 + u) * C + c) * HW + hw) : 0.f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (n0 + u >= nimg) break;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (cd1) {
+          s1[q] = dadd(s1[q], (double)v[u][q]);
+          s2[q] = dadd(s2[q], dmul((double)(n0 + u), (double)v[u][q]));
+        }
+        t[lane][warp + 8 * q] = v[u][q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pl = warp + 8 * q, sp = blockIdx.x * 32 + pl;
+        if (sp < HW) Dt[((long long)(n0 + u) * HW + sp) * C + c0 + lane] = t[pl][lane];
+      }
+      __syncthreads();
+    }
+  }
+  if (cd1 && ok) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long e = (long long)(c0 + warp + 8 * q) * HW + hw;
+      cd1[e] = s1[q];
+      cd2[e] = s2[q];
+    }
+  }
+}
+
 int g_num_sms = 0;
 
-template <int BN, int MODE, bool FUSE>
+template <int BN, int MODE, bool FUSE, bool GROUPED>
 int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024));
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE, FUSE, GROUPED>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  FTC_LAUNCH(k_conv_tc<BN, MODE, FUSE><<<grid, kThreads, smem, s>>>(a, tm));
+  FTC_LAUNCH(k_conv_tc<BN, MODE, FUSE, GROUPED><<<grid, kThreads, smem, s>>>(a, tm));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -920,11 +985,12 @@ int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cud
 }  // namespace
 
 bool tc_supported(const ftc_conv_desc& d) {
-  if (d.groups != 1) return false;
+  if (d.groups < 1 || d.C % d.groups || d.M % d.groups) return false;
   if (d.R > 15) return false;  // tap validity bits: rows 0-14, columns 16-30
-  const long long K = (long long)d.C * d.R * d.R;
+  const long long Ckw = d.C / d.groups, Mg = d.M / d.groups;
+  const long long K = Ckw * d.R * d.R;
   const long long nkc = (K + kBK - 1) / kBK;
-  const long long bn = d.M <= 128 ? ((d.M + 31) / 32) * 32 : 128;
+  const long long bn = Mg <= 128 ? ((Mg + 31) / 32) * 32 : 128;
   if (1024 + stages_host(bn) * bn * 256 + nkc * kBK * 8 + 512 > 227 * 1024) return false;
   if ((long long)d.C * d.H * d.H >= (1LL << 31)) return false;
   const long long E = (d.H + 2LL * d.pad - d.R) / d.stride + 1;
@@ -935,40 +1001,45 @@ bool tc_supported(const ftc_conv_desc& d) {
 int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cudaStream_t s) {
   TcPlan* p = new TcPlan();
   p->M = d.M;
-  p->K = d.C * d.R * d.R;
+  p->groups = d.groups;
+  p->Ckw = d.C / d.groups;
+  p->Mg = d.M / d.groups;
+  p->Ctot = d.C;
+  p->K = p->Ckw * d.R * d.R;
   p->nkc = (p->K + kBK - 1) / kBK;
   // main accumulator drained every 2 K chunks (64 K): the tensor core truncates its
   // accumulator adds, so longer runs lose accuracy (G=3 already exceeds the reference's
   // own FP32 error on ResNet-18's 1x1 projections); G=1 costs ~9% more on AlexNet conv2
   p->G = 2;
   if (const char* g = getenv("FTC_TC_DRAIN_CHUNKS")) p->G = atoi(g) > 0 ? atoi(g) : 1;
-  if (d.M <= 128) {
-    p->BN = ((d.M + 31) / 32) * 32;
-    p->ntiles = 1;
+  if (p->Mg <= 128) {
+    p->BN = ((p->Mg + 31) / 32) * 32;
+    p->ntg = 1;
   } else {
     p->BN = 128;
-    p->ntiles = (d.M + 127) / 128;
+    p->ntg = (p->Mg + 127) / 128;
   }
   // channel-last gather: faster producers, but with the MMA issue chain the bottleneck it
   // does not pay for its transpose pass yet (AlexNet conv2 669 vs 641 us): opt-in
   // K order: tap-major (k = (i*R + j)*C + c) for the channel-last paths
   const bool corners_ok = d.pad <= 127 && d.pad - (d.R - 1) >= -128 && d.stride <= 8;
-  p->im2col = d.C % 32 == 0 && corners_ok && !getenv("FTC_TC_NO_TMA") && !getenv("FTC_TC_NHWC");
-  p->nhwc = !p->im2col && d.C % 32 == 0 && getenv("FTC_TC_NHWC") != nullptr;
+  p->im2col = p->Ckw % 32 == 0 && corners_ok && !getenv("FTC_TC_NO_TMA") && !getenv("FTC_TC_NHWC");
+  p->nhwc = !p->im2col && d.groups == 1 && d.C % 32 == 0 && getenv("FTC_TC_NHWC") != nullptr;
   if (const char* bn = getenv("FTC_TC_MAX_BN")) {  // experimentation: cap the N tile
     const int cap = atoi(bn);
     if ((cap == 32 || cap == 64 || cap == 96 || cap == 128) && p->BN > cap) {
       p->BN = cap;
-      p->ntiles = (d.M + cap - 1) / cap;
+      p->ntg = (p->Mg + cap - 1) / cap;
     }
   }
+  p->ntiles = p->groups * p->ntg;
   const size_t n = (size_t)p->ntiles * p->nkc * 2 * p->BN * kBK;
   if (cudaMalloc(&p->Wp, n * sizeof(float)) != cudaSuccess) {
     delete p;
     set_error(FTC_CUDA_ERROR, "cudaMalloc(packed W) failed");
     return FTC_CUDA_ERROR;
   }
-  FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, d.M, p->K, p->BN, p->ntiles, p->nkc, d.C, d.R * d.R,
+  FTC_LAUNCH(k_pack_w<<<592, 256, 0, s>>>(W_dev, p->Wp, p->Mg, p->ntg, p->K, p->BN, p->ntiles, p->nkc, p->Ckw, d.R * d.R,
                                          (p->nhwc || p->im2col) ? 1 : 0));
   if (cudaMalloc(&p->tab, (size_t)p->nkc * kBK * sizeof(int2)) != cudaSuccess) {
     cudaFree(p->Wp);
@@ -1025,7 +1096,7 @@ int tc_plan_create(const ftc_conv_desc& d, const float* W_dev, TcPlan** out, cud
       return FTC_CUDA_ERROR;
     }
   } else {
-    FTC_LAUNCH(k_build_tab<<<(p->nkc * kBK + 255) / 256, 256, 0, s>>>(p->tab, d.C, d.H, d.R, p->K,
+    FTC_LAUNCH(k_build_tab<<<(p->nkc * kBK + 255) / 256, 256, 0, s>>>(p->tab, p->Ckw, d.H, d.R, p->K,
                                                                      p->nkc * kBK));
   }
   cudaError_t e = cudaGetLastError();
@@ -1059,7 +1130,8 @@ bool tc_co5_in_kernel(const TcPlan* p, int N, int E) {
   const long long E2 = (long long)E * E;
   const long long grid = 148;
   const long long pos = (E2 + grid - 1) / grid;
-  const long long rounds = pos * ((p->K + 32LL * kCkUnroll - 1) / (32LL * kCkUnroll));
+  const long long Kc = (long long)p->K * p->groups;  // Co5 taps run over all channels
+  const long long rounds = pos * ((Kc + 32LL * kCkUnroll - 1) / (32LL * kCkUnroll));
   const long long tiles = ((long long)N * E2 + kBM - 1) / kBM * p->ntiles;
   const long long conv = (tiles + grid - 1) / grid * p->nkc * 1000LL;
   return rounds * 700LL * 4 <= conv;
@@ -1080,6 +1152,12 @@ int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg,
   if (!cd1) {  // transpose only: parallel over images too
     const dim3 tg((unsigned)((HW + 31) / 32), (unsigned)(C / 32), (unsigned)nimg);
     FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(D, Dt, C, HW, n_lo));
+    FTC_CUDA_CHECK(cudaGetLastError());
+    return FTC_OK;
+  }
+  if (n_lo == 0) {
+    const dim3 g((unsigned)((HW + 31) / 32), (unsigned)(C / 32));
+    FTC_LAUNCH(k_nhwc_cd32<<<g, 256, 0, s>>>(D, Dt, C, HW, nimg, cd1, cd2));
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }
@@ -1108,6 +1186,9 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   a.nkc = p->nkc;
   a.BN = p->BN;
   a.ntiles = p->ntiles;
+  a.Ckw = p->Ckw;
+  a.Mg = p->Mg;
+  a.ntg = p->ntg;
   a.G = p->G;
   const long long E2 = (long long)c.E * c.E;
   a.P = (long long)c.N * E2;
@@ -1159,13 +1240,18 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
     }
     a.fd = *c.fd;
   }
-#define FTC_BN_SWITCH(MODE, FUSE)                                                  \
-  switch (p->BN) {                                                                 \
-    case 32: return launch_bn<32, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
-    case 64: return launch_bn<64, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
-    case 96: return launch_bn<96, MODE, FUSE>(a, p->tmA, grid, smem, s);           \
-    case 128: return launch_bn<128, MODE, FUSE>(a, p->tmA, grid, smem, s);         \
+#define FTC_BN_SWITCH(MODE, FUSE)                                                            \
+  switch (p->BN) {                                                                           \
+    case 32: return grouped ? launch_bn<32, MODE, FUSE, true>(a, p->tmA, grid, smem, s)       \
+                            : launch_bn<32, MODE, FUSE, false>(a, p->tmA, grid, smem, s);     \
+    case 64: return grouped ? launch_bn<64, MODE, FUSE, true>(a, p->tmA, grid, smem, s)       \
+                            : launch_bn<64, MODE, FUSE, false>(a, p->tmA, grid, smem, s);     \
+    case 96: return grouped ? launch_bn<96, MODE, FUSE, true>(a, p->tmA, grid, smem, s)       \
+                            : launch_bn<96, MODE, FUSE, false>(a, p->tmA, grid, smem, s);     \
+    case 128: return grouped ? launch_bn<128, MODE, FUSE, true>(a, p->tmA, grid, smem, s)     \
+                             : launch_bn<128, MODE, FUSE, false>(a, p->tmA, grid, smem, s);   \
   }
+  const bool grouped = p->groups > 1;
   if (p->im2col) {
     if (fuse) {
       FTC_BN_SWITCH(2, true)
@@ -1173,7 +1259,12 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
       FTC_BN_SWITCH(2, false)
     }
   } else if (p->nhwc) {
-    FTC_BN_SWITCH(1, false)
+    switch (p->BN) {
+      case 32: return launch_bn<32, 1, false, false>(a, p->tmA, grid, smem, s);
+      case 64: return launch_bn<64, 1, false, false>(a, p->tmA, grid, smem, s);
+      case 96: return launch_bn<96, 1, false, false>(a, p->tmA, grid, smem, s);
+      case 128: return launch_bn<128, 1, false, false>(a, p->tmA, grid, smem, s);
+    }
   } else if (fuse) {
     FTC_BN_SWITCH(0, true)
   } else {

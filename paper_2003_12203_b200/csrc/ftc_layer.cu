@@ -1013,13 +1013,18 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
         L->ck_exact = false;
       }
     }
+    // Co5 in the conv's checksum warp when it fits in the conv's shadow, else in the
+    // CoC-D kernel after the conv (one launch either way)
     const bool co5_in = tc_co5_in_kernel(L->tc, d.N, L->E);
-    if (!co5_in) CK(launch_co5_sliced(cd1_use, L->cw1, L->co5f, d.C, d.H, d.R, d.stride, d.pad, L->E, s));
     FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
                    L->fstats_hd, co5_in ? cd1_use : nullptr, L->co5tab};
     CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready));
-    CK(launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats,
-                           L->fticket, L->fstats_hd, s));
+    if (co5_in)
+      CK(launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats,
+                             L->fticket, L->fstats_hd, s));
+    else
+      CK(launch_co5_detect(cd1_use, L->cw1, L->co5f, L->so5acc, d.N, d.C, d.H, d.R, d.stride, d.pad, L->E,
+                           d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats, L->fticket, L->fstats_hd, s));
     FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
     L->inflight = true;
     return FTC_OK;

@@ -165,3 +165,41 @@ def test_glue_tile_cd1(N, C, H, act, k, s, p):
     assert L.ftc_glue_act_pool_cd1(x.data_ptr(), out.data_ptr(), None, N, C, H, act, k, s, p, None, st) == 0
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,C,H,M,R,s,p,G", [(2, 64, 12, 96, 3, 1, 1, 2), (3, 128, 9, 64, 3, 2, 1, 4),
+                                             (2, 96, 11, 48, 1, 1, 0, 3), (2, 12, 10, 24, 3, 1, 1, 3),
+                                             (1, 256, 7, 512, 3, 1, 1, 2)])
+def test_grouped_conv_on_tensor_cores(N, C, H, M, R, s, p, G):
+    """Grouped layers run on the tensor-core engines (TMA im2col when C/groups % 32 == 0,
+    register gather otherwise): output vs conv_forward<float>, and a protected call with an
+    output flip gives run_protected_layer<double>'s verdict."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import synth
+    D = synth.relu_like((N, C, H, H), 3)
+    W = synth.he_normal(M, C // G, R, 4)
+    B = synth.uniform((M,), -0.1, 0.1, 5)
+    prm = F.ConvParams(stride=s, pad=p, groups=G, bias_enabled=True)
+    L = F.ProtectedConv(W, B, prm, N, H)
+    Dg = torch.from_numpy(D).cuda()
+    Og = L.conv_forward(Dg).cpu().numpy()
+    d = O.dims(N, C, H, M, R, s, p, G, True)
+    Or = O.conv_f32(d, D, W, B)
+    assert _rel(Og, Or).max() <= 1e-5
+    plan = F.LayerPlan(rc_enabled=True, clc_enabled=True, tau=1e-3)
+    O0, rep = L.protected(Dg, plan)
+    assert not rep.detected and torch.equal(O0.cpu(), torch.from_numpy(Og))
+    E = Og.shape[-1]
+    for t, (n, m, x, y, bit) in enumerate([(0, M - 1, 0, 0, 27), (N - 1, M // G, E - 1, E // 2, 29)]):
+        Of, r = L.protected(Dg, plan, [F.output_bitflip(n, m, x, y, bit)])
+        Os = Og.copy()
+        Os[n, m, x, y] = synth.flip32(Os[n, m, x, y], bit)
+        ref = O.protected_layer(d, D, W, B, True, True, 1e-3, O_conv=Os)
+        got = r.verdict()
+        for k in ("detected", "stage", "stages_attempted"):
+            assert got[k] == ref[k], (t, k, got, ref)
+        if got["stage"] in ("coc", "rc", "clc", "fc", "recompute"):
+            assert np.array_equal(Of.cpu().numpy(), Og)
+    L.close()
