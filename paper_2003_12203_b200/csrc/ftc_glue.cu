@@ -125,12 +125,12 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
 
 // k_act_pool_t over a group of images per block, also summing each thread's (c, position)
 // over the group in FP64 into the Cd1 workspace (the consumer conv's clean-path Cd1)
-template <int KT>
+template <int KT, int ACT>
 __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict__ in, float* __restrict__ out,
                                                        float* __restrict__ out_t, int N, int NG, int C, int H,
-                                                       int act, int kr, int s, int p, int Ho, double* __restrict__ ws,
+                                                       int kr, int s, int p, int Ho, double* __restrict__ ws,
                                                        long long tick_off, long long slab_off) {
-  __shared__ float tile[8][33];
+  __shared__ float tile[2][8][33];
   const int k = KT > 0 ? KT : kr;
   const int plane = Ho * Ho;
   const int tid = threadIdx.x;
@@ -141,52 +141,81 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
   const int g = blockIdx.z, G = gridDim.z;
   const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
   const bool ok = pos < plane;
+  // window origin and its valid rows / columns, fixed across images (no per-tap bounds
+  // arithmetic in the image loop)
   int x0 = 0, y0 = 0;
+  uint32_t rmask = 0, cmask = 0;
   if (ok) {
     const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
     x0 = ox * s - p;
     y0 = oy * s - p;
+    for (int i = 0; i < k && i < 32; ++i) {
+      if ((unsigned)(x0 + i) < (unsigned)H) rmask |= 1u << i;
+      if ((unsigned)(y0 + i) < (unsigned)H) cmask |= 1u << i;
+    }
   }
-  double acc = 0.0;
-  for (int n = n_lo; n < n_hi; ++n) {
+  const long long HH = (long long)H * H;
+  const float* src = in + ((long long)n_lo * C + c) * HH + (long long)x0 * H + y0;
+  float* op = out + ((long long)n_lo * C + c) * plane + pos;
+  float* tp = out_t ? out_t + ((long long)n_lo * plane + spos) * C + blockIdx.y * 32 + wc : nullptr;
+  const long long istep = (long long)C * HH, ostep = (long long)C * plane;
+  auto pool = [&](const float* sp) -> float {
     float m = -INFINITY;
+    if constexpr (KT > 0) {
+      float v[KT * KT];
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) v[i * KT + j] = ((rmask >> i) & (cmask >> j) & 1u) ? __ldg(sp + i * H + j) : 0.f;
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+          if ((rmask >> i) & (cmask >> j) & 1u) m = fmaxf(m, act_fn(v[i * KT + j], ACT));
+    } else {
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j)
+          if ((rmask >> i) & (cmask >> j) & 1u) m = fmaxf(m, act_fn(__ldg(sp + i * H + j), ACT));
+    }
+    return m;
+  };
+  double acc = 0.0;
+  int n = n_lo;
+  for (; n + 2 <= n_hi; n += 2) {  // two images' windows in flight
+    float m0 = -INFINITY, m1 = -INFINITY;
     if (ok) {
-      const float* src = in + ((long long)n * C + c) * H * H;
-      if constexpr (KT > 0) {
-        float v[KT * KT];
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-#pragma unroll
-          for (int j = 0; j < KT; ++j) {
-            const int x = x0 + i, y = y0 + j;
-            v[i * KT + j] = (x >= 0 && x < H && y >= 0 && y < H) ? __ldg(src + x * H + y) : 0.f;
-          }
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-#pragma unroll
-          for (int j = 0; j < KT; ++j) {
-            const int x = x0 + i, y = y0 + j;
-            if (x >= 0 && x < H && y >= 0 && y < H) m = fmaxf(m, act_fn(v[i * KT + j], act));
-          }
-      } else {
-        for (int i = 0; i < k; ++i) {
-          const int x = x0 + i;
-          if (x < 0 || x >= H) continue;
-          for (int j = 0; j < k; ++j) {
-            const int y = y0 + j;
-            if (y < 0 || y >= H) continue;
-            m = fmaxf(m, act_fn(__ldg(src + x * H + y), act));
-          }
-        }
-      }
-      out[((long long)n * C + c) * plane + pos] = m;
-      acc += (double)m;
+      m0 = pool(src);
+      m1 = pool(src + istep);
+      op[0] = m0;
+      op[ostep] = m1;
+      acc += (double)m0;
+      acc += (double)m1;
     }
     if (out_t) {
-      tile[pl][cl] = m;
+      tile[0][pl][cl] = m0;
+      tile[1][pl][cl] = m1;
       __syncthreads();
-      if (spos < plane) out_t[((long long)n * plane + spos) * C + blockIdx.y * 32 + wc] = tile[wp][wc];
+      if (spos < plane) {
+        tp[0] = tile[0][wp][wc];
+        tp[(long long)plane * C] = tile[1][wp][wc];
+      }
       __syncthreads();
+    }
+    src += 2 * istep;
+    op += 2 * ostep;
+    if (tp) tp += 2LL * plane * C;
+  }
+  if (n < n_hi) {
+    float m0 = -INFINITY;
+    if (ok) {
+      m0 = pool(src);
+      op[0] = m0;
+      acc += (double)m0;
+    }
+    if (out_t) {
+      tile[0][pl][cl] = m0;
+      __syncthreads();
+      if (spos < plane) tp[0] = tile[0][wp][wc];
     }
   }
   const long long per = (long long)C * plane;
@@ -409,15 +438,20 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
   const int G = act_pool_groups(N, C, Ho);
   const int NG = (N + G - 1) / G;
   const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
-#define FTC_APT(KT)                                                                                   \
-  FTC_LAUNCH(k_act_pool_t_cd1<KT><<<g, 256, 0, st>>>(in, out, out_t, N, NG, C, H, act, k, s, p, Ho, ws, \
-                                                      w.tick_off, w.slab_off))
+#define FTC_APT2(KT, ACT) \
+  FTC_LAUNCH(k_act_pool_t_cd1<KT, ACT><<<g, 256, 0, st>>>(in, out, out_t, N, NG, C, H, k, s, p, Ho, ws, w.tick_off, \
+                                                           w.slab_off))
+#define FTC_APT(KT)                  \
+  if (act == 1) FTC_APT2(KT, 1);      \
+  else if (act == 2) FTC_APT2(KT, 2); \
+  else FTC_APT2(KT, 0)
   switch (k) {
     case 1: FTC_APT(1); break;
     case 2: FTC_APT(2); break;
     case 3: FTC_APT(3); break;
     default: FTC_APT(0); break;
   }
+#undef FTC_APT2
 #undef FTC_APT
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
