@@ -263,10 +263,9 @@ def main():
         wl.e2e_stream(2)
     torch.cuda.synchronize()
 
-    # ---- protected, inputs resident in HBM: device time of the clean path
-    for L in wl.layers:
-        lib.ftc_layer_set_timing(L.h, 1)
-        lib.ftc_layer_kernel_time(L.h, None, None, 1)
+    # ---- protected, inputs resident in HBM: device time of the clean path (no per-kernel
+    # instrumentation here: event records between launches would cut the programmatic
+    # dependent launches; the conv kernel times come from a second pass below)
     from paper_2003_12203_b200 import dist as ftc_dist
     reports = []
     verdict_tables = []
@@ -299,6 +298,18 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = lib.ftc_kernel_launches() - l0
+    t_prot = tot / args.steps
+
+    # ---- roofline pass: the same K protected steps with CUDA events bracketing every
+    # conv launch on its stream (ftc_layer_set_timing)
+    for L in wl.layers:
+        lib.ftc_layer_set_timing(L.h, 1)
+        lib.ftc_layer_kernel_time(L.h, None, None, 1)
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        wl.launch()
+        wl.finish()
+    torch.cuda.synchronize()
     conv_ms = []
     for L in wl.layers:
         import ctypes as C
@@ -306,7 +317,6 @@ def main():
         lib.ftc_layer_kernel_time(L.h, C.byref(ms), C.byref(n), 1)
         conv_ms.append((ms.value, n.value))
         lib.ftc_layer_set_timing(L.h, 0)
-    t_prot = tot / args.steps
 
     # ---- unprotected conv stack (same kernels, no ABFT) for the overhead
     t_unprot = timed(wl.unprotected, args.steps) / args.steps
@@ -364,6 +374,7 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (5 conv launches)",
                 "kernel": "conv (sum over layers per step)",
                 "kernel_ms_per_step": conv_avg_ms, "peak_basis": basis,
+                "kernel_timing": "CUDA events around each conv launch, second pass of K protected steps",
                 "flops_per_step": wl.flops}
         cpu = None
         if not args.no_cpu_baseline and world == 1:

@@ -433,6 +433,8 @@ __global__ void k_co5_taps(const double* __restrict__ cw1, int C, int H, int R, 
 __global__ void __launch_bounds__(256) k_detect_fused(const double* __restrict__ co5, double* __restrict__ so5,
                                                      int N, int E2, int bias, const double* agg, double tau,
                                                      DetectStats* st, unsigned int* ticket, DetectStats* host_out) {
+  pdl_trigger();
+  pdl_wait();
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   int bad = 0;
   unsigned long long devb = 0ull;
@@ -484,6 +486,8 @@ __global__ void __launch_bounds__(256) k_co5_detect(const double* __restrict__ c
                                                    const double* agg, double tau, DetectStats* st,
                                                    unsigned int* ticket, DetectStats* host_out) {
   __shared__ double red[256];
+  pdl_trigger();
+  pdl_wait();
   const int R = RT > 0 ? RT : Rrt, RR = R * R, E2 = E * E, S = 256 / P;
   const int t = threadIdx.x, pl = t % P, sl = t / P;
   const int f = blockIdx.x * P + pl;
@@ -676,19 +680,19 @@ int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double*
   while (P > 1 && (E2 + P - 1) / P < 2 * 148 * 4 && 256 / P < C) P >>= 1;
   const int g = (E2 + P - 1) / P;
   if (R == 3)
-    FTC_LAUNCH(k_co5_detect<3><<<g, 256, 0, s>>>(cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg, tau, st,
-                                                 ticket, host_out));
+    FTC_LAUNCH_PDL(k_co5_detect<3>, dim3(g), dim3(256), 0, s, cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg,
+                   tau, st, ticket, host_out);
   else
-    FTC_LAUNCH(k_co5_detect<0><<<g, 256, 0, s>>>(cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg, tau, st,
-                                                 ticket, host_out));
+    FTC_LAUNCH_PDL(k_co5_detect<0>, dim3(g), dim3(256), 0, s, cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg,
+                   tau, st, ticket, host_out);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
 
 int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
                         DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s) {
-  FTC_LAUNCH(k_detect_fused<<<blocks_for(E2), kThreads, 0, s>>>(co5, so5, N, E2, bias, agg, tau, st, ticket,
-                                                                host_out));
+  FTC_LAUNCH_PDL(k_detect_fused, dim3(blocks_for(E2)), dim3(kThreads), 0, s, co5, so5, N, E2, bias, agg, tau, st, ticket,
+                 host_out);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

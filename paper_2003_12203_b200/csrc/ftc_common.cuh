@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/ftc_abi.h"
 
@@ -35,6 +36,36 @@ void count_launch();
     __VA_ARGS__;            \
     ::ftc::count_launch();  \
   } while (0)
+
+// Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous
+// kernel on the stream drains; it runs griddepcontrol.wait before touching memory the
+// previous kernel produced.  Off with FTC_NO_PDL=1 (A/B experiments).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#define FTC_LAUNCH_PDL(kernel, grid, block, smem, stream, ...)                        \
+  do {                                                                                 \
+    FTC_CUDA_CHECK(::ftc::launch_pdl(kernel, grid, block, smem, stream, __VA_ARGS__)); \
+    ::ftc::count_launch();                                                             \
+  } while (0)
+
+// device side of PDL: wait for the previous grid's completion (and memory), and let the
+// next grid launch (no-ops without the launch attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ------------------------------------------------------------------ device helpers
 // FP64 arithmetic of the checksum path goes through the _rn intrinsics so nvcc can

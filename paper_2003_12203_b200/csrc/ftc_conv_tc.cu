@@ -334,6 +334,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel's tail; the next kernel (the
+  // CoC-D compare or glue) may be scheduled now -- it cannot share an SM with this CTA
+  // and waits for this grid before reading anything
+  pdl_trigger();
+  pdl_wait();
   const uint32_t corr_col = (uint32_t)(2 * BN);  // correction accumulator (per tile)
   const uint32_t a_col0 = (uint32_t)(3 * BN);
 
@@ -862,6 +867,7 @@ __global__ void k_build_tab_nhwc(int2* tab, int C, int H, int R, int nkc) {
 __global__ void __launch_bounds__(256) k_nchw_to_nhwc(const float* __restrict__ D, float* __restrict__ Dt, int C,
                                                      int HW, int n_lo) {
   __shared__ float t[32][33];
+  pdl_wait();
   const long long n = n_lo + blockIdx.z;
   const int hw0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   const float* src = D + n * C * HW;
@@ -923,6 +929,7 @@ __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, 
                                                   int HW, int nimg, double* __restrict__ cd1,
                                                   double* __restrict__ cd2) {
   __shared__ float t[32][33];
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hw = blockIdx.x * 32 + lane;
   const bool ok = hw < HW;
@@ -957,6 +964,7 @@ __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, 
       __syncthreads();
     }
   }
+  pdl_trigger();
   if (cd1 && ok) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -977,7 +985,7 @@ int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cud
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  FTC_LAUNCH(k_conv_tc<BN, MODE, FUSE, GROUPED><<<grid, kThreads, smem, s>>>(a, tm));
+  FTC_LAUNCH_PDL(k_conv_tc<BN, MODE, FUSE, GROUPED>, dim3(grid), dim3(kThreads), smem, s, a, tm);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -1151,13 +1159,13 @@ int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg,
   }
   if (!cd1) {  // transpose only: parallel over images too
     const dim3 tg((unsigned)((HW + 31) / 32), (unsigned)(C / 32), (unsigned)nimg);
-    FTC_LAUNCH(k_nchw_to_nhwc<<<tg, dim3(32, 8), 0, s>>>(D, Dt, C, HW, n_lo));
+    FTC_LAUNCH_PDL(k_nchw_to_nhwc, tg, dim3(32, 8), 0, s, D, Dt, C, HW, n_lo);
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }
   if (n_lo == 0) {
     const dim3 g((unsigned)((HW + 31) / 32), (unsigned)(C / 32));
-    FTC_LAUNCH(k_nhwc_cd32<<<g, 256, 0, s>>>(D, Dt, C, HW, nimg, cd1, cd2));
+    FTC_LAUNCH_PDL(k_nhwc_cd32, g, dim3(256), 0, s, D, Dt, C, HW, nimg, cd1, cd2);
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }

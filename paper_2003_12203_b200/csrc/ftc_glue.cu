@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256) k_act_pool_flat(const float* __restrict__
                                                       unsigned total, int H, int Ho, int act, int kr, int s, int p) {
   const int k = KT > 0 ? KT : kr;
   const unsigned plane = (unsigned)(Ho * Ho);
+  pdl_wait();
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const unsigned pl = e / plane, pos = e - pl * plane;
     const int ox = (int)(pos / (unsigned)Ho), oy = (int)pos - ox * Ho;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y, G = gridDim.y;
   const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
+  pdl_wait();
   if (e < per) {
     double a = 0.0;
     int n = n_lo;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
     for (; n < n_hi; ++n) a += (double)__ldcs(D + (long long)n * per + e);
     ws[slab_off + per * g + e] = a;
   }
+  pdl_trigger();
   if (ws_arrive(ws, tick_off, blockIdx.x, G)) {
     if (e < per) {
       double t = 0.0;
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
     }
   }
   const long long HH = (long long)H * H;
+  pdl_wait();
   const float* src = in + ((long long)n_lo * C + c) * HH + (long long)x0 * H + y0;
   float* op = out + ((long long)n_lo * C + c) * plane + pos;
   float* tp = out_t ? out_t + ((long long)n_lo * plane + spos) * C + blockIdx.y * 32 + wc : nullptr;
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
       if (spos < plane) tp[0] = tile[0][wp][wc];
     }
   }
+  pdl_trigger();
   const long long per = (long long)C * plane;
   const long long e = (long long)c * plane + pos;
   if (ok) ws[slab_off + per * g + e] = acc;
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(256) k_act_pool_tile(const float* __restrict__
     }
   }
   const long long HH = (long long)H * H;
+  pdl_wait();
   {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -311,7 +317,7 @@ int launch_act_pool(const float* in, float* out, int NC, int H, int act, int k, 
     if (blocks > 148LL * 64) blocks = 148LL * 64;
     const float* ip = in + p0 * H * H;
     float* op = out + p0 * plane;
-#define FTC_APF(KT) FTC_LAUNCH(k_act_pool_flat<KT><<<(unsigned)blocks, 256, 0, st>>>(ip, op, tot, H, Ho, act, k, s, p))
+#define FTC_APF(KT) FTC_LAUNCH_PDL(k_act_pool_flat<KT>, dim3((unsigned)blocks), dim3(256), 0, st, ip, op, tot, H, Ho, act, k, s, p)
     switch (k) {
       case 1: FTC_APF(1); break;
       case 2: FTC_APF(2); break;
@@ -405,7 +411,7 @@ int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C
   const int Ho = (H + 2 * p - k) / s + 1;
   const dim3 g((unsigned)((Ho * Ho + 31) / 32), (unsigned)((C + 31) / 32), (unsigned)N);
 #define FTC_APT(KT) \
-  FTC_LAUNCH(k_act_pool_tile<KT><<<g, 256, 0, st>>>(in, out, out_t, C, H, act, k, s, p, Ho))
+  FTC_LAUNCH_PDL(k_act_pool_tile<KT>, g, dim3(256), 0, st, in, out, out_t, C, H, act, k, s, p, Ho)
   switch (k) {
     case 1: FTC_APT(1); break;
     case 2: FTC_APT(2); break;
@@ -422,7 +428,7 @@ int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStrea
   const int G = cd1_parts_groups(N, per);
   const int NG = (N + G - 1) / G;
   const dim3 g((unsigned)((per + 255) / 256), (unsigned)((N + NG - 1) / NG));
-  FTC_LAUNCH(k_cd1_parts<<<g, 256, 0, st>>>(D, N, per, NG, ws, w.tick_off, w.slab_off));
+  FTC_LAUNCH_PDL(k_cd1_parts, g, dim3(256), 0, st, D, N, per, NG, ws, w.tick_off, w.slab_off);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -439,8 +445,8 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
   const int NG = (N + G - 1) / G;
   const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
 #define FTC_APT2(KT, ACT) \
-  FTC_LAUNCH(k_act_pool_t_cd1<KT, ACT><<<g, 256, 0, st>>>(in, out, out_t, N, NG, C, H, k, s, p, Ho, ws, w.tick_off, \
-                                                           w.slab_off))
+  FTC_LAUNCH_PDL(k_act_pool_t_cd1<KT, ACT>, g, dim3(256), 0, st, in, out, out_t, N, NG, C, H, k, s, p, Ho, ws, \
+                 w.tick_off, w.slab_off)
 #define FTC_APT(KT)                  \
   if (act == 1) FTC_APT2(KT, 1);      \
   else if (act == 2) FTC_APT2(KT, 2); \

@@ -36,6 +36,11 @@ void set_error(int code, const std::string& msg) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = getenv("FTC_NO_PDL") == nullptr;
+  return on;
+}
+
 }  // namespace ftc
 
 using namespace ftc;

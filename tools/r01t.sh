@@ -1,0 +1,12 @@
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r01t_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r01t_pytest.log; tail -3 gpurun_out/r01t_pytest.log
+TAG=pdl python tools/layer_times.py 2>&1 | tail -2
+FTC_NO_PDL=1 TAG=nopdl python tools/layer_times.py 2>&1 | tail -2
+TAG=pdl python tools/layer_times.py 2>&1 | tail -2
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/r01t_alex.json 2> gpurun_out/r01t_alex.err
+timeout 300 python bench.py --workload config1 --no-cpu-baseline > gpurun_out/r01t_c1.json 2> gpurun_out/r01t_c1.err
+python - <<'PY'
+import json
+for f in ("gpurun_out/r01t_alex.json","gpurun_out/r01t_c1.json"):
+    d=json.loads(open(f).read().strip().splitlines()[-1])
+    print(f, d["value"], "ovh%", round(d["abft_overhead_pct"],2), "ms", d["ms_per_step"], "unprot", d["ms_per_step_unprotected"], "frac", round(d["roofline"]["frac"],3), "e2e", d["e2e"]["value"])
+PY
