@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256) k_co5_adapt(const double* __restrict__ cd
   }
 }
 
-__global__ void __launch_bounds__(256) k_detect_adapt(const double* __restrict__ co5,
+__global__ void __launch_bounds__(256) k_detect_adapt(double* __restrict__ co5,
                                                      const double* __restrict__ rowsum, int parts, int N, int E2,
                                                      int bias, const double* agg, double tau, DetectStats* st,
                                                      unsigned int* ticket, DetectStats* host_out, int P) {
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(256) k_detect_adapt(const double* __restrict__
       for (int q = 0; q < S; ++q) ss += red[q * P + pp];
       if (bias) ss -= (double)N * agg[0];
       const double c = co5[ff];
+      co5[ff] = 0.0;  // keep the clean-path Co5 buffer zero between calls
       double den = fabs(c);
       if (den < fabs(ss)) den = fabs(ss);
       if (den < 1.0) den = 1.0;
@@ -430,7 +431,7 @@ __global__ void k_co5_taps(const double* __restrict__ cw1, int C, int H, int R, 
 // bias not yet removed), Co5 by its checksum warp.  One thread per position compares
 // them (values_differ, checksums.hpp:54-60) and re-zeroes So5; the last block publishes
 // {flagged, max_rel_dev} into the mapped host record and re-arms the counters.
-__global__ void __launch_bounds__(256) k_detect_fused(const double* __restrict__ co5, double* __restrict__ so5,
+__global__ void __launch_bounds__(256) k_detect_fused(double* __restrict__ co5, double* __restrict__ so5,
                                                      int N, int E2, int bias, const double* agg, double tau,
                                                      DetectStats* st, unsigned int* ticket, DetectStats* host_out) {
   pdl_trigger();
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(256) k_detect_fused(const double* __restrict__
     so5[f] = 0.0;
     if (bias) ss -= (double)N * agg[0];
     const double c = __ldcg(co5 + f);
+    co5[f] = 0.0;  // Co5 may have been scattered (staging pass): re-arm it too
     double den = fabs(c);
     if (den < fabs(ss)) den = fabs(ss);
     if (den < 1.0) den = 1.0;
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(256) k_co5_detect(const double* __restrict__ c
   if (t < P && f < E2) {
     double c = 0.0;
     for (int q = 0; q < S; ++q) c += red[q * P + t];
-    co5[f] = c;
+    co5[f] = 0.0;  // the clean-path Co5 buffer is zero between calls (the staging pass scatters into it)
     double ss = __ldcg(so5 + f);
     so5[f] = 0.0;
     if (bias) ss -= (double)N * agg[0];
@@ -661,7 +663,7 @@ int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, 
   return FTC_OK;
 }
 
-int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+int launch_detect_so5(double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                       const double* agg, double tau, DetectStats* st, unsigned int* ticket,
                       DetectStats* host_out, cudaStream_t s) {
   const int P = pick_positions(N * parts);
@@ -689,7 +691,7 @@ int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double*
   return FTC_OK;
 }
 
-int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
+int launch_detect_fused(double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
                         DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s) {
   FTC_LAUNCH_PDL(k_detect_fused, dim3(blocks_for(E2)), dim3(kThreads), 0, s, co5, so5, N, E2, bias, agg, tau, st, ticket,
                  host_out);

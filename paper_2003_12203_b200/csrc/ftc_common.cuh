@@ -206,8 +206,13 @@ bool tc_co5_in_kernel(const TcPlan* p, int N, int E);  // fused path: Co5 by the
 float* tc_nhwc_buffer(const TcPlan* p);    // its NHWC input copy
 // D (NCHW) -> Dt (NHWC) for images [n_lo, n_lo + nimg); with cd1 != null also the exact
 // input checksums Cd1/Cd2 (n ascending, FP64; whole batch only: n_lo = 0, nimg = N)
+struct Co5Job {  // have the staging pass also produce Co5 = Cd1 (*) Cw1 (co5 zero on entry)
+  double* co5;
+  const double* cw1;
+  int H, R, U, pad, E;
+};
 int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg, double* cd1, double* cd2,
-                   cudaStream_t s);  // N-tiles = row-sum partial slabs of N*E2
+                   cudaStream_t s, const Co5Job* co5 = nullptr);  // N-tiles = row-sum partial slabs of N*E2
 
 // ------------------------------------------------------------------ checksum kernels
 // input_checksums (exact order)
@@ -239,7 +244,7 @@ int launch_cd1_fast(const float* D, int N, long long per, double* cd1, cudaStrea
 // clean path: Cd1 = sum_n D_n in FP64, any order, through a workspace [Cd1][tickets]
 // [partial slabs over image groups] (zero-filled once; the kernels re-arm the tickets).
 // The act+pool glue kernels write the next layer's Cd1 the same way.
-int launch_detect_fused(const double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
+int launch_detect_fused(double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
                         DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s);
 int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double* so5, int N, int C, int H, int R,
                       int U, int pad, int E, int bias, const double* agg, double tau, DetectStats* st,
@@ -255,7 +260,7 @@ int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C
 // (host_out) and re-zeroes st/ticket for the next call
 int launch_co5_sliced(const double* cd1, const double* cw1, double* co5, int C, int H, int R, int U,
                       int pad, int E, cudaStream_t s);
-int launch_detect_so5(const double* co5, const double* rowsum, int parts, int N, int E2, int bias,
+int launch_detect_so5(double* co5, const double* rowsum, int parts, int N, int E2, int bias,
                       const double* agg, double tau, DetectStats* st, unsigned int* ticket,
                       DetectStats* host_out, cudaStream_t s);
 int launch_detect_exact(const double* co5, const double* so5, int E2, double tau, uint8_t* mask,

@@ -922,30 +922,39 @@ __global__ void __launch_bounds__(256) k_nhwc_cd(const float* __restrict__ D, fl
 }
 
 // k_nhwc_cd with 32-channel x 32-position tiles: warp w loads channels w, w+8, w+16,
-// w+24 (lane = position, 128-byte rows) for 4 images at a time (16 loads in flight per
+// w+24 (lane = position, 128-byte rows) for 8 images at a time (32 loads in flight per
 // thread), accumulates the exact-order checksums of its 4 (c, position) items over n
 // ascending, and writes each image's tile channel-last through shared memory.
+struct Co5Scatter {  // optional: the block's share of Co5 = Cd1 (*) Cw1, scattered (FP64 atomics)
+  double* co5;         // [E][E], zero on entry (the CoC-D kernel re-zeroes it)
+  const double* cw1;   // [C][R][R]
+  int H, R, U, pad, E;
+};
+
 __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, float* __restrict__ Dt, int C,
                                                   int HW, int nimg, double* __restrict__ cd1,
-                                                  double* __restrict__ cd2) {
+                                                  double* __restrict__ cd2, Co5Scatter sc) {
   __shared__ float t[32][33];
+  constexpr int kScTaps = 9;
+  __shared__ double red[kScTaps][8][32];
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hw = blockIdx.x * 32 + lane;
   const bool ok = hw < HW;
   const int c0 = blockIdx.y * 32;
+  constexpr int kImg = 8;  // images' loads in flight per thread (32 loads)
   double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
-  for (int n0 = 0; n0 < nimg; n0 += 4) {
-    float v[4][4];
+  for (int n0 = 0; n0 < nimg; n0 += kImg) {
+    float v[kImg][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kImg; ++u)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = c0 + warp + 8 * q;
         v[u][q] = (ok && n0 + u < nimg) ? __ldg(D + ((long long)(n0 + u) * C + c) * HW + hw) : 0.f;
       }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kImg; ++u) {
       if (n0 + u >= nimg) break;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -971,6 +980,36 @@ __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, 
       const long long e = (long long)(c0 + warp + 8 * q) * HW + hw;
       cd1[e] = s1[q];
       cd2[e] = s2[q];
+    }
+  }
+  if (sc.co5) {
+    // Co5 is linear in Cd1: this block's 32 channels x 32 input positions contribute
+    // sum_c Cd1[c][h][w] * Cw1[c][i][j] to output (x, y) with x*U + i - pad = h (same for
+    // y, j); channels are summed through shared memory, one atomic per (position, tap)
+    const int RR = sc.R * sc.R;
+    const int h = hw / sc.H, w = hw - (hw / sc.H) * sc.H;
+    for (int t0 = 0; t0 < RR; t0 += kScTaps) {  // kScTaps taps per round, one barrier each
+      const int nt = min(kScTaps, RR - t0);
+      for (int tt = 0; tt < nt; ++tt) {
+        double part = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) part += s1[q] * sc.cw1[(c0 + warp + 8 * q) * RR + t0 + tt];
+        red[tt][warp][lane] = part;
+      }
+      __syncthreads();
+      for (int tt = warp; tt < nt; tt += 8) {  // warp per tap: channel sum, one atomic per position
+        if (!ok) continue;
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) v += red[tt][ww][lane];
+        const int tap = t0 + tt, i = tap / sc.R, j = tap - (tap / sc.R) * sc.R;
+        const int xs = h + sc.pad - i, ys = w + sc.pad - j;
+        if (xs >= 0 && ys >= 0 && xs % sc.U == 0 && ys % sc.U == 0) {
+          const int x = xs / sc.U, y = ys / sc.U;
+          if (x < sc.E && y < sc.E) atomicAdd(sc.co5 + x * sc.E + y, v);
+        }
+      }
+      __syncthreads();
     }
   }
 }
@@ -1147,7 +1186,7 @@ bool tc_co5_in_kernel(const TcPlan* p, int N, int E) {
 float* tc_nhwc_buffer(const TcPlan* p) { return p ? p->Dt : nullptr; }
 
 int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg, double* cd1, double* cd2,
-                   cudaStream_t s) {
+                   cudaStream_t s, const Co5Job* co5) {
   if (C % 32) {
     set_error(FTC_CONFIG_ERROR, "launch_nhwc_cd: C % 32 != 0");
     return FTC_CONFIG_ERROR;
@@ -1165,7 +1204,9 @@ int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg,
   }
   if (n_lo == 0) {
     const dim3 g((unsigned)((HW + 31) / 32), (unsigned)(C / 32));
-    FTC_LAUNCH_PDL(k_nhwc_cd32, g, dim3(256), 0, s, D, Dt, C, HW, nimg, cd1, cd2);
+    Co5Scatter sc{};
+    if (co5 && cd1) sc = Co5Scatter{co5->co5, co5->cw1, co5->H, co5->R, co5->U, co5->pad, co5->E};
+    FTC_LAUNCH_PDL(k_nhwc_cd32, g, dim3(256), 0, s, D, Dt, C, HW, nimg, cd1, cd2, sc);
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }

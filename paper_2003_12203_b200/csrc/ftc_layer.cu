@@ -783,7 +783,9 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
       (st = dalloc(&L->cd2, L->nCd)) || (st = dalloc(&L->co5f, L->E2)) ||
       (st = dalloc(&L->so5acc, L->E2)) || (st = dalloc(&L->stats, 1)))
     return fail(st);
-  if (cudaMemset(L->so5acc, 0, L->E2 * sizeof(double)) != cudaSuccess) return fail(FTC_CUDA_ERROR);
+  if (cudaMemset(L->so5acc, 0, L->E2 * sizeof(double)) != cudaSuccess ||
+      cudaMemset(L->co5f, 0, L->E2 * sizeof(double)) != cudaSuccess)  // Co5 may be scattered into
+    return fail(FTC_CUDA_ERROR);
   {
     // Cd1 workspace of the fused clean path when no producer supplies Cd1
     const long long n = cd1_ws_doubles(desc->N, L->nCd);
@@ -994,7 +996,7 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
   // accumulates So5 from its row sums; one small kernel then runs CoC-D.
   static const bool fused_off = getenv("FTC_NO_FUSED") != nullptr;
   if (!fused_off && use_tc(L) && !pre_faults) {
-    bool dt_ready = false;
+    bool dt_ready = false, co5_ready = false;
     if (cd1_in) {
       cd1_use = cd1_in;
       if (cd2_in) {  // exact-order checksums: kept for the error path
@@ -1007,8 +1009,11 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     } else {
       const bool stage = tc_im2col(L->tc) && !(L->nhwc_ready && L->D_staged == D);
       if (stage && d.N <= 32) {
-        // small batch: one pass writes the NHWC copy and the exact-order Cd1/Cd2
-        CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s));
+        // small batch: one pass writes the NHWC copy, the exact-order Cd1/Cd2 and, by
+        // linearity, Co5 (each block scatters its Cd1 elements' share)
+        const Co5Job job{L->co5f, L->cw1, d.H, d.R, d.stride, d.pad, L->E};
+        CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s, &job));
+        co5_ready = true;
         dt_ready = true;
         cd1_use = L->cd1;
         L->ck_exact = true;
@@ -1020,11 +1025,11 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     }
     // Co5 in the conv's checksum warp when it fits in the conv's shadow, else in the
     // CoC-D kernel after the conv (one launch either way)
-    const bool co5_in = tc_co5_in_kernel(L->tc, d.N, L->E);
+    const bool co5_in = !co5_ready && tc_co5_in_kernel(L->tc, d.N, L->E);
     FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
                    L->fstats_hd, co5_in ? cd1_use : nullptr, L->co5tab};
     CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready));
-    if (co5_in)
+    if (co5_in || co5_ready)
       CK(launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats,
                              L->fticket, L->fstats_hd, s));
     else

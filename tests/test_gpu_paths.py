@@ -203,3 +203,30 @@ def test_grouped_conv_on_tensor_cores(N, C, H, M, R, s, p, G):
         if got["stage"] in ("coc", "rc", "clc", "fc", "recompute"):
             assert np.array_equal(Of.cpu().numpy(), Og)
     L.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,C,H,M", [(4, 32, 14, 40), (16, 64, 56, 64), (8, 16, 12, 24), (40, 32, 10, 32)])
+def test_clean_path_state_across_paths(N, C, H, M):
+    """The clean path keeps its device state (Co5 / So5 accumulators, counters) re-armed
+    whichever variant a call takes -- Co5 scattered by the staging pass (small batches),
+    computed in the conv or after it, or the side-stream path a pre_conv fault selects:
+    clean calls interleaved with faulted ones never report a detection."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import synth
+    D = synth.relu_like((N, C, H, H), 21)
+    W = synth.he_normal(M, C, 3, 22)
+    L = F.ProtectedConv(W, None, F.ConvParams(pad=1), N, H)
+    Dg = torch.from_numpy(D).cuda()
+    plan = F.LayerPlan(rc_enabled=True, clc_enabled=True, tau=1e-3)
+    O0, r = L.protected(Dg, plan)
+    assert not r.detected
+    seq = [[], [F.Fault("fmap", 1, 2, 3, 4, "add", 0, 5.0)], [], [F.output_bitflip(0, 1, 2, 3, 29)], [],
+           [F.Fault("fmap", 0, 0, 0, 0, "add", 0, 7.0)], [], []]
+    for k, faults in enumerate(seq):
+        O, r = L.protected(Dg, plan, faults)
+        if not faults:
+            assert not r.detected, (k, r.verdict())
+            assert torch.equal(O, O0)
+    L.close()
