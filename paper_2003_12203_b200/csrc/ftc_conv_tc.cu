@@ -496,6 +496,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         const long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
         const int n0 = (int)(p0 / E2), f0 = (int)(p0 % E2);
         const int cw = (f0 % E) * a.U - a.pad, ch = (f0 / E) * a.U - a.pad;
+        if constexpr (MODE == 0) {
+          // register-gather layers: L2-prefetch the input rows this CTA's NEXT tile gathers
+          // (its window rows of every channel, one bulk prefetch per channel) a tile ahead,
+          // so its compulsory misses hit L2 instead of DRAM
+          const int tn = t + (int)gridDim.x;
+          if (tn < ntile_total && a.C <= 16) {
+            const long long q0 = (long long)(a.pt_lo + tn % a.npt) * kBM;
+            const long long q1 = min(q0 + kBM, a.P) - 1;
+            const int m0 = (int)(q0 / E2), m1 = (int)(q1 / E2);
+            for (int nn = m0; nn <= m1; ++nn) {
+              const int xa = nn == m0 ? (int)(q0 % E2) / E : 0, xb = nn == m1 ? (int)(q1 % E2) / E : E - 1;
+              const int ha = max(0, xa * a.U - a.pad), hb = min(H - 1, xb * a.U - a.pad + R - 1);
+              if (ha > hb) continue;
+              for (int c = 0; c < a.C; ++c) {
+                const float* rb = a.D + ((long long)nn * a.C + c) * HH + (long long)ha * H;
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(rb) & ~(uintptr_t)15;
+                const uintptr_t hi = (reinterpret_cast<uintptr_t>(rb + (long long)(hb - ha + 1) * H) + 15) &
+                                     ~(uintptr_t)15;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo))
+                             : "memory");
+              }
+            }
+          }
+        }
         int ti = 0, tj = 0, cb = 0;  // K chunk kc = ((ti*R + tj)*ncb + cb)
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
           if constexpr (TMAA) {
