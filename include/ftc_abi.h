@@ -297,6 +297,13 @@ int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const floa
                            const ftc_grad_fault* hook, int32_t n_hook, float* dW, float* dD,
                            ftc_backward_report* report, void* stream);
 
+/* host-buffer forms of the two (copies in, device pass, copies out; synchronous) */
+int ftc_conv_backward_host(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, float* dW,
+                           float* dD, void* stream);
+int ftc_protected_backward_host(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO,
+                                double tau, const ftc_grad_fault* hook, int32_t n_hook, float* dW, float* dD,
+                                ftc_backward_report* report, void* stream);
+
 /* Seeded uniform draws exactly as Tensor4<T>::random (tensor.hpp:57-66) and
  * random_weights (model_io.cpp:176-192): std::mt19937_64(seed) through
  * std::uniform_real_distribution<double>(lo, hi), n values into out (host memory). */

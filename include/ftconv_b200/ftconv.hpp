@@ -19,6 +19,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../ftc_abi.h"
@@ -200,6 +201,46 @@ inline Tensor4 run_protected_layer(const Tensor4& D_in, const Tensor4& W_golden,
   detail::fill_report(r, rep);
   check(st, "run_protected_layer");
   return O;
+}
+
+/// BackwardReport (workflow.hpp:343-347)
+struct BackwardReport {
+  bool dw_detected = false;
+  bool dd_detected = false;
+  bool recomputed = false;
+};
+
+/// conv_backward (conv.hpp:150-185): host D/W/dO in, (dW, dD) out; FP64-accumulated.
+inline std::pair<Tensor4, Tensor4> conv_backward(const Tensor4& D, const Tensor4& W, const Tensor4& dO,
+                                                 const ConvParams& p) {
+  if (p.groups != 1) throw ConfigError("grouped back-propagation is unsupported");
+  ConvParams q = p;
+  q.bias_enabled = false;
+  const ftc_conv_desc d = detail::make_desc(D, W, q);
+  Tensor4 dW(W.dim(0), W.dim(1), W.dim(2), W.dim(3)), dD(D.dim(0), D.dim(1), D.dim(2), D.dim(3));
+  check(ftc_conv_backward_host(&d, D.data(), W.data(), dO.data(), dW.data(), dD.data(), nullptr), "conv_backward");
+  return {std::move(dW), std::move(dD)};
+}
+
+/// run_protected_backward (workflow.hpp:350-417); `hook` replaces the post_hook callback
+/// (applied to the first pass only).  Throws IntegrityError if the recompute fails.
+inline std::pair<Tensor4, Tensor4> run_protected_backward(const Tensor4& D, const Tensor4& W, const Tensor4& dO,
+                                                          const ConvParams& p, double tau, BackwardReport& rep,
+                                                          const std::vector<ftc_grad_fault>& hook = {}) {
+  if (p.groups != 1) throw ConfigError("grouped back-propagation is unsupported");
+  ConvParams q = p;
+  q.bias_enabled = false;
+  const ftc_conv_desc d = detail::make_desc(D, W, q);
+  Tensor4 dW(W.dim(0), W.dim(1), W.dim(2), W.dim(3)), dD(D.dim(0), D.dim(1), D.dim(2), D.dim(3));
+  ftc_backward_report r{};
+  const int st = ftc_protected_backward_host(&d, D.data(), W.data(), dO.data(), tau,
+                                             hook.empty() ? nullptr : hook.data(), (int32_t)hook.size(),
+                                             dW.data(), dD.data(), &r, nullptr);
+  rep.dw_detected = r.dw_detected != 0;
+  rep.dd_detected = r.dd_detected != 0;
+  rep.recomputed = r.recomputed != 0;
+  check(st, "run_protected_backward");
+  return {std::move(dW), std::move(dD)};
 }
 
 /// A protected layer bound to a batch size: keeps W, Cw1/Cw2 and the packed

@@ -29,6 +29,7 @@ EXPORTS = (
     "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
     "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
+    "ftc_conv_backward_host", "ftc_protected_backward_host",
 )
 
 

@@ -304,4 +304,52 @@ int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const floa
   return st;
 }
 
+// host-buffer forms (the reference's calling convention): copies in, device pass, copies out
+static int bwd_host(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, float* dW, float* dD,
+                    bool prot, double tau, const ftc_grad_fault* hook, int32_t n_hook, ftc_backward_report* rep,
+                    void* stream) {
+  Bwd b;
+  int st = validate_bwd(desc, &b);
+  if (st != FTC_OK) return st;
+  if (!D || !W || !dO || !dW || !dD) {
+    set_error(FTC_INVALID_ARGUMENT, "null argument");
+    return FTC_INVALID_ARGUMENT;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nW = b.nW * sizeof(float), nD = b.nD * sizeof(float), nO = (size_t)b.N * b.M * b.E2 * sizeof(float);
+  float *d_D = nullptr, *d_W = nullptr, *d_O = nullptr, *d_dW = nullptr, *d_dD = nullptr;
+  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_D, nD, s));
+  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_W, nW, s));
+  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_O, nO, s));
+  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_dW, nW, s));
+  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_dD, nD, s));
+  FTC_CUDA_CHECK(cudaMemcpyAsync(d_D, D, nD, cudaMemcpyHostToDevice, s));
+  FTC_CUDA_CHECK(cudaMemcpyAsync(d_W, W, nW, cudaMemcpyHostToDevice, s));
+  FTC_CUDA_CHECK(cudaMemcpyAsync(d_O, dO, nO, cudaMemcpyHostToDevice, s));
+  st = prot ? ftc_protected_backward(desc, d_D, d_W, d_O, tau, hook, n_hook, d_dW, d_dD, rep, stream)
+            : ftc_conv_backward(desc, d_D, d_W, d_O, d_dW, d_dD, stream);
+  if (st == FTC_OK) {
+    cudaMemcpyAsync(dW, d_dW, nW, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(dD, d_dD, nD, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(d_D, s); cudaFreeAsync(d_W, s); cudaFreeAsync(d_O, s); cudaFreeAsync(d_dW, s); cudaFreeAsync(d_dD, s);
+  FTC_CUDA_CHECK(cudaStreamSynchronize(s));
+  return st;
+}
+
+int ftc_conv_backward_host(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, float* dW,
+                           float* dD, void* stream) {
+  return bwd_host(desc, D, W, dO, dW, dD, false, 0.0, nullptr, 0, nullptr, stream);
+}
+
+int ftc_protected_backward_host(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO,
+                                double tau, const ftc_grad_fault* hook, int32_t n_hook, float* dW, float* dD,
+                                ftc_backward_report* report, void* stream) {
+  if (!report) {
+    set_error(FTC_INVALID_ARGUMENT, "null report");
+    return FTC_INVALID_ARGUMENT;
+  }
+  return bwd_host(desc, D, W, dO, dW, dD, true, tau, hook, n_hook, report, stream);
+}
+
 }  // extern "C"

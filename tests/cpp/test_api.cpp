@@ -98,6 +98,30 @@ int main() {
     Tensor4 O4 = layer(D, plan, r4, {f});
     CHECK(r4.stage == ResolveStage::coc && O4.raw() == ref.raw());
   }
+  {  // test_conv.cpp:149-158 / test_workflow.cpp:276-309: back-propagation
+    ConvParams p;
+    Tensor4 D(1, 1, 1, 1), W(1, 1, 1, 1), dO(1, 1, 1, 1);
+    D(0, 0, 0, 0) = 3;
+    W(0, 0, 0, 0) = 5;
+    dO(0, 0, 0, 0) = 7;
+    auto g = conv_backward(D, W, dO, p);
+    CHECK(g.first(0, 0, 0, 0) == 21 && g.second(0, 0, 0, 0) == 35);
+    Tensor4 D2(2, 2, 5, 5), W2(3, 2, 2, 2), O2(2, 3, 4, 4);
+    for (std::size_t i = 0; i < D2.size(); ++i) D2.raw()[i] = (float)std::sin(0.1 * i);
+    for (std::size_t i = 0; i < W2.size(); ++i) W2.raw()[i] = (float)std::cos(0.3 * i);
+    for (std::size_t i = 0; i < O2.size(); ++i) O2.raw()[i] = (float)std::sin(0.7 * i + 1);
+    auto clean = conv_backward(D2, W2, O2, p);
+    BackwardReport br;
+    auto pg = run_protected_backward(D2, W2, O2, p, 1e-10, br);
+    CHECK(!br.dw_detected && !br.dd_detected && !br.recomputed);
+    CHECK(pg.first.raw() == clean.first.raw() && pg.second.raw() == clean.second.raw());
+    BackwardReport bw;
+    auto fg = run_protected_backward(D2, W2, O2, p, 1e-10, bw, {{0, 1, 8, 3.0}});  // dW(1,0,0,0) += 3
+    CHECK(bw.dw_detected && bw.recomputed && fg.first.raw() == clean.first.raw());
+    BackwardReport bd;
+    auto dg = run_protected_backward(D2, W2, O2, p, 1e-10, bd, {{1, 1, 37, -4.0}});  // dD(0,1,2,2) -= 4
+    CHECK(bd.dd_detected && bd.recomputed && dg.second.raw() == clean.second.raw());
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

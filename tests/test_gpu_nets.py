@@ -173,3 +173,48 @@ def test_host_pipeline_matches_serial_forward(depth):
     pn.close()
     if pn2:
         pn2.close()
+
+
+@pytest.mark.parametrize("layer", ["c10", "c21"])
+def test_yolo_multi_flip_patterns(layer):
+    """BASELINE config 5's multi-error injection on real YOLOv2 activations (batch 2):
+    up to 3 flips per layer across images / filters -- one per column (RC), one per row
+    (ClC), and clustered ones (FC / recompute) -- with the verdict of
+    run_protected_layer<double> on the same FP32 output, and a repaired output equal to
+    the fault-free one."""
+    import paper_2003_12203_b200 as F
+    torch = _torch()
+    net, pn = build("yolov2", 2)
+    pn.forward()
+    torch.cuda.synchronize()
+    opc, Cin, H, E = [c for c in pn.convs if c[0].dst == layer][0]
+    D = pn.buf[opc.src].cpu().numpy()
+    W, b = pn.weights[layer]
+    L = pn.layers[layer]
+    Oclean = pn.buf[layer].cpu().numpy()
+    plan = pn.plans[layer]
+    M = opc.M
+    patterns = [
+        [(0, 3, 1, 2, 28), (1, 40, 5, 7, 27), (0, M - 1, E - 1, 0, 29)],     # distinct filters
+        [(0, 9, 2, 2, 28), (1, 9, 3, 3, 26)],                                # one filter, two images
+        [(1, 5, 0, 0, 27), (1, 6, 1, 1, 28), (1, 7, 2, 2, 29)],              # one image, three filters
+        [(0, 1, 1, 1, 28), (0, 2, 1, 1, 28), (1, 1, 1, 1, 28)],              # clustered
+    ]
+    stages = set()
+    for pat in patterns:
+        faults = [F.output_bitflip(n, m, x, y, bit) for n, m, x, y, bit in pat]
+        Og, rep = L.protected(pn.buf[opc.src], plan, faults)
+        Of = Oclean.copy()
+        for n, m, x, y, bit in pat:
+            Of[n, m, x, y] = synth.flip32(Of[n, m, x, y], bit)
+        ref = O.protected_layer(O.dims(2, Cin, H, M, opc.R, opc.stride, opc.pad, 1, opc.bias), D, W, b,
+                                plan.rc_enabled, plan.clc_enabled, plan.tau, O_conv=Of)
+        got = rep.verdict()
+        for k in ("detected", "stage", "stages_attempted", "weights_reloaded", "recomputed"):
+            assert got[k] == ref[k], (pat, k, got, ref)
+        assert [tuple(t) for t in got["corrected_blocks"]] == [tuple(t) for t in ref["corrected_blocks"]]
+        if got["stage"] in ("coc", "rc", "clc", "fc", "recompute"):
+            assert np.array_equal(Og.cpu().numpy(), Oclean)
+        stages.add(got["stage"])
+    assert len(stages) >= 2, stages
+    pn.close()
