@@ -251,6 +251,11 @@ int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double*
                       unsigned int* ticket, DetectStats* host_out, cudaStream_t s);
 int launch_co5_taps(const double* cw1, int C, int H, int R, Co5Tap* taps, cudaStream_t s);
 long long cd1_ws_doubles(int N, long long per);
+long long cd1_ws_doubles_g(int N, int C, int Ho, long long per);  // also covers the glue kernels' layout
+// act + pool (k x k, stride s, pad p) with NHWC staging (out_t) and the consumer's Cd1 in
+// ws; out (NCHW) may be NULL (staging pass of a caller-supplied D: act 0, k = s = 1)
+int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k,
+                             int s, int p, double* ws, cudaStream_t st);
 // C, Ho: the pooling producer's shape when the workspace is shared with it (0, 0: none)
 int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStream_t s, int C = 0, int Ho = 0);
 int launch_act_pool_nhwc(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k, int s,

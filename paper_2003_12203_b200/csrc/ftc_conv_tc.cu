@@ -81,7 +81,10 @@ constexpr int stages_for() {
   return BN >= 128 ? 2 : (BN >= 96 ? 3 : 4);
 }
 constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
-constexpr int kAS = 4;                       // MODE 2 shared-memory A stages
+#ifndef FTC_KAS
+#define FTC_KAS 4
+#endif
+constexpr int kAS = FTC_KAS;                 // MODE 2 shared-memory A stages
 constexpr uint32_t kAStageBytes = 128u * 128u;  // 128 pixels x 32 FP32 channels
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
 constexpr int kLoaderWarp = 8;
@@ -147,6 +150,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// off the MMA-critical path (epilogue, B loader): back off between polls so the spinning
+// warps leave issue slots to the producers and the MMA issuers
+#ifndef FTC_WAIT_NS
+#define FTC_WAIT_NS 64
+#endif
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (FTC_WAIT_NS > 0) __nanosleep(FTC_WAIT_NS);
   }
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -523,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         int ti = 0, tj = 0, cb = 0;  // K chunk kc = ((ti*R + tj)*ncb + cb)
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
           if constexpr (TMAA) {
-            mbar_wait(emptyAs0 + 8 * sa, pha ^ 1u);
+            mbar_wait_lazy(emptyAs0 + 8 * sa, pha ^ 1u);
             if (a.dbg & 1) {  // profiling: skip the A gather
               mbar_arrive(fullAs0 + 8 * sa);
             } else {
@@ -539,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           }
           const uint32_t s = sB, ph = phB;
           if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
-          mbar_wait(emptyB0 + 8 * s, ph ^ 1u);
+          mbar_wait_lazy(emptyB0 + 8 * s, ph ^ 1u);
           TC_TRACE((a.dbg & 64) && blockIdx.x == 0, 8, g);
           if (a.dbg & 16) {
             mbar_arrive(fullB0 + 8 * s);
@@ -705,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       for (int jj = 0; jj < HALF; ++jj) sum[jj] = acc_t(0);
       for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
         const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
-        mbar_wait(accf0 + 8 * acc, aph);
+        mbar_wait_lazy(accf0 + 8 * acc, aph);
         TC_TRACE(eprof, 6, gc);
         tc_after();
         const uint32_t base = tmem + lane_off + acc * (uint32_t)BN + (uint32_t)(half * HALF);
@@ -724,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         TC_TRACE(eprof, 7, gc);
       }
       // the tile's correction accumulator
-      mbar_wait(corrf, tl & 1u);
+      mbar_wait_lazy(corrf, tl & 1u);
       tc_after();
       const uint32_t cbase = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
 #pragma unroll

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
   const long long HH = (long long)H * H;
   pdl_wait();
   const float* src = in + ((long long)n_lo * C + c) * HH + (long long)x0 * H + y0;
-  float* op = out + ((long long)n_lo * C + c) * plane + pos;
+  float* op = out ? out + ((long long)n_lo * C + c) * plane + pos : nullptr;
   float* tp = out_t ? out_t + ((long long)n_lo * plane + spos) * C + blockIdx.y * 32 + wc : nullptr;
   const long long istep = (long long)C * HH, ostep = (long long)C * plane;
   auto pool = [&](const float* sp) -> float {
@@ -190,8 +190,10 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
     if (ok) {
       m0 = pool(src);
       m1 = pool(src + istep);
-      op[0] = m0;
-      op[ostep] = m1;
+      if (out) {  // out == NULL: staging pass of a caller-supplied D (NHWC + Cd1 only)
+        op[0] = m0;
+        op[ostep] = m1;
+      }
       acc += (double)m0;
       acc += (double)m1;
     }
@@ -206,14 +208,14 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
       __syncthreads();
     }
     src += 2 * istep;
-    op += 2 * ostep;
+    if (op) op += 2 * ostep;
     if (tp) tp += 2LL * plane * C;
   }
   if (n < n_hi) {
     float m0 = -INFINITY;
     if (ok) {
       m0 = pool(src);
-      op[0] = m0;
+      if (out) op[0] = m0;
       acc += (double)m0;
     }
     if (out_t) {

@@ -788,7 +788,7 @@ int ftc_layer_create(const ftc_conv_desc* desc, const float* W_host, const float
     return fail(FTC_CUDA_ERROR);
   {
     // Cd1 workspace of the fused clean path when no producer supplies Cd1
-    const long long n = cd1_ws_doubles(desc->N, L->nCd);
+    const long long n = cd1_ws_doubles_g(desc->N, desc->C, desc->H, L->nCd);
     if ((st = dalloc(&L->cd1ws, (size_t)n)) || (st = dalloc(&L->co5tab, (size_t)L->nCw))) return fail(st);
     if (cudaMemset(L->cd1ws, 0, (size_t)n * sizeof(double)) != cudaSuccess) return fail(FTC_CUDA_ERROR);
   }
@@ -1017,6 +1017,13 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
         dt_ready = true;
         cd1_use = L->cd1;
         L->ck_exact = true;
+      } else if (stage) {
+        // larger batches: one pass parallel over image groups stages the NHWC copy and
+        // reduces the any-order Cd1 (the exact-order checksums wait for the error path)
+        CK(launch_act_pool_nhwc_cd1(D, nullptr, tc_nhwc_buffer(L->tc), d.N, d.C, d.H, 0, 1, 1, 0, L->cd1ws, s));
+        dt_ready = true;
+        cd1_use = L->cd1ws;
+        L->ck_exact = false;
       } else {
         CK(launch_cd1_parts(D, d.N, L->nCd, L->cd1ws, s));
         cd1_use = L->cd1ws;
