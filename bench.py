@@ -338,6 +338,30 @@ def main():
         e1.synchronize()
         t_e2e = e0.elapsed_time(e1) / args.steps
 
+    # ---- faulted forwards (BASELINE: one seeded output bit flip per layer): detection,
+    # localisation, repair and downstream replay on the device, timed end to end
+    faulted = None
+    if hasattr(wl, "faulted"):
+        runs, stages, t_f, repaired_ok, repaired_runs = 3, {}, 0.0, True, 0
+        for r in range(runs):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            reps_f, same = wl.faulted(r)
+            torch.cuda.synchronize()
+            t_f += time.perf_counter() - t0
+            for rep in reps_f:
+                stages[rep.stage] = stages.get(rep.stage, 0) + 1
+            # a sub-threshold (undetected) or discarded flip stays in the output by design;
+            # when every layer repaired its flip the net output must be the fault-free one
+            if all(rep.stage in ("coc", "rc", "clc", "fc", "recompute") for rep in reps_f):
+                repaired_runs += 1
+                repaired_ok = repaired_ok and same
+        faulted = {"ms_per_forward": 1e3 * t_f / runs, "runs": runs, "flips_per_forward": len(wl.layers),
+                   "stages": stages, "fully_repaired_runs": repaired_runs,
+                   "fully_repaired_output_equals_fault_free": repaired_ok,
+                   "timing": "host wall clock around forward (launch + verdicts + repairs + replays)"}
+
     # max over ranks
     tt = torch.tensor([t_prot, t_unprot, t_e2e, t_e2e_serial], dtype=torch.float64, device=dev)
     detected = sum(1 for reps in reports for r in reps if r.detected)
@@ -395,7 +419,8 @@ def main():
             "config": {"workload": workload_name(args.workload), "global_batch": images,
                        "per_gpu_batch": wl.batch, "engine": args.engine,
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every step",
-                       "plan": "rc+clc on, per-layer tau"},
+                       "plan": "rc+clc on, per-layer tau",
+                       "tau_per_layer": getattr(wl, "taus", None)},
             "abft_overhead_pct": overhead, "ms_per_step_unprotected": t_unprot,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": images / (t_e2e / 1e3), "unit": "images/s",
@@ -405,6 +430,7 @@ def main():
                     "serial_value": images / (t_e2e_serial / 1e3)},
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
             "clocks": clocks, "detections_in_timed_region": detected,
+            "faulted_forward": faulted,
         }
         print(json.dumps(line))
     if world > 1:

@@ -511,6 +511,22 @@ class BenchNet:
         self.pn.torch.cuda.current_stream().synchronize()
         return list(reps.values())
 
+    def faulted(self, run: int):
+        """One protected forward with one seeded output bit flip (bits 20-30) in every conv
+        (BASELINE configs: "one seeded output bit-flip per layer") -> (verdicts, output
+        equals the fault-free one)."""
+        from .ftconv import output_bitflip
+        if not hasattr(self, "clean_out"):
+            self.pn.forward()
+            self.clean_out = self.pn.output().clone()
+        faults = {}
+        for li, (op, Cin, H, E) in enumerate(self.pn.convs):
+            n, m, x, y, bit = synth.flip_sample(9000 + li, run, self.batch, op.M, E)
+            faults[op.dst] = [output_bitflip(n, m, x, y, bit)]
+        reps = self.pn.forward(faults)
+        same = bool(self.pn.torch.equal(self.pn.output(), self.clean_out))
+        return list(reps.values()), same
+
     def e2e_stream(self, steps, before_step=None, start_event=None):
         """`steps` host batches through HostPipeline (H2D/D2H overlapped with compute)."""
         if not hasattr(self, "pipe"):
