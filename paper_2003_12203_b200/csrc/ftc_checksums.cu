@@ -204,22 +204,17 @@ __global__ void k_sum_rows(VirtualO v, int N, int M, int E2, uint32_t which, con
   if (which & FTC_CK_O4) so4[q] = s4;
 }
 
-// So5/So6/So7 (per position, (n,m) ascending) (checksums.hpp:224-229)
-__global__ void k_sum_total(VirtualO v, int N, int M, int E2, uint32_t which, const double* agg,
-                            double* so5, double* so6, double* so7) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= E2) return;
-  double s5 = 0.0, s6 = 0.0, s7 = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double wn = (double)n;
-    const long long base = (long long)n * M * E2 + f;
-    for (int m = 0; m < M; ++m) {
-      const double x = vo(v, base + (long long)m * E2);
-      s5 = dadd(s5, x);
-      s6 = dadd(s6, dmul((double)m, x));
-      s7 = dadd(s7, dmul(wn, x));
-    }
-  }
+// So5/So6/So7 with a warp per position (warp_seq_sums567): one thread per position
+// walking the N*M terms with dependent loads took ~10 ms per call on AlexNet's layers.
+__global__ void __launch_bounds__(256) k_sum_total_warp(VirtualO v, int N, int M, int E2, uint32_t which,
+                                                       const double* agg, double* so5, double* so6, double* so7) {
+  __shared__ double buf[8][2 * kSeqBatch];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (f >= E2) return;  // whole warps exit together
+  double s5, s6, s7;
+  warp_seq_sums567([&](long long q) { return vo(v, q * E2 + f); }, (long long)N * M, M, buf[w], s5, s6, s7);
+  if (lane != 0) return;
   if (agg) {
     const double nN = (double)N, wnn = (double)((long long)N * (N - 1) / 2);
     s5 = dsub(s5, dmul(nN, agg[0]));
@@ -633,8 +628,8 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
                                                                    bias ? agg : nullptr, so[1],
                                                                    so[3]));
   if (which & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7))
-    FTC_LAUNCH(k_sum_total<<<blocks_for(E2, 64), 64, 0, s>>>(v, N, M, E2, which, bias ? agg : nullptr, so[4],
-                                                  so[5], so[6]));
+    FTC_LAUNCH(k_sum_total_warp<<<blocks_for((long long)E2 * 32), kThreads, 0, s>>>(
+        v, N, M, E2, which, bias ? agg : nullptr, so[4], so[5], so[6]));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -296,21 +296,20 @@ __global__ void k_verify_apply(Patches p, int np, int M, int E2, const float* O,
   }
 }
 
-// fresh So5/So6/So7 where touched, cached elsewhere; compare (workflow.hpp:209-211)
-__global__ void k_verify_pos(Fam F, unsigned trusted, const float* O, int N, int M, int E2,
-                             int bias, const double* agg, double tau, VerifyWS ws, int32_t* fail) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= E2) return;
+// fresh So5/So6/So7 where touched, cached elsewhere; compare (workflow.hpp:209-211).
+// A warp per position: touched positions re-sum the (n, m) sequence with
+// warp_seq_sums567 (a thread walking N*M dependent loads made each verify ~18 ms).
+__global__ void __launch_bounds__(256) k_verify_pos(Fam F, unsigned trusted, const float* O, int N, int M, int E2,
+                                                   int bias, const double* agg, double tau, VerifyWS ws,
+                                                   int32_t* fail) {
+  __shared__ double buf[8][2 * kSeqBatch];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (f >= E2) return;  // whole warps exit together
   double s5, s6, s7;
   if (ws.touched5[f]) {
-    s5 = s6 = s7 = 0.0;
-    for (int n = 0; n < N; ++n)
-      for (int m = 0; m < M; ++m) {
-        const double x = vo(O, ws.ov, ws.present, ((long long)n * M + m) * E2 + f);
-        s5 = dadd(s5, x);
-        s6 = dadd(s6, dmul((double)m, x));
-        s7 = dadd(s7, dmul((double)n, x));
-      }
+    warp_seq_sums567([&](long long q) { return vo(O, ws.ov, ws.present, q * E2 + f); }, (long long)N * M, M,
+                     buf[w], s5, s6, s7);
     if (bias) {
       const double nN = (double)N, wn = (double)((long long)N * (N - 1) / 2);
       s5 = dsub(s5, dmul(nN, agg[0]));
@@ -322,6 +321,7 @@ __global__ void k_verify_pos(Fam F, unsigned trusted, const float* O, int N, int
     s6 = (trusted & FTC_CK_O6) ? F.s[5][f] : 0.0;
     s7 = (trusted & FTC_CK_O7) ? F.s[6][f] : 0.0;
   }
+  if (lane != 0) return;
   bool bad = false;
   if ((trusted & FTC_CK_O5) && values_differ(F.c[4][f], s5, tau)) bad = true;
   if ((trusted & FTC_CK_O6) && values_differ(F.c[5][f], s6, tau)) bad = true;
@@ -470,7 +470,7 @@ int run_verify(const Fam& F, unsigned trusted, const float* O, int N, int M, int
     count_launch();
   }
   if (trusted & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7))
-    FTC_LAUNCH(k_verify_pos<<<(E2 + 63) / 64, 64, 0, s>>>(F, trusted, O, N, M, E2, bias, agg, tau, ws, fail));
+    FTC_LAUNCH(k_verify_pos<<<(E2 + 7) / 8, 256, 0, s>>>(F, trusted, O, N, M, E2, bias, agg, tau, ws, fail));
   if (trusted & (FTC_CK_O1 | FTC_CK_O3))
     FTC_LAUNCH(k_verify_col<<<(int)(((long long)M * E2 + kT - 1) / kT), kT, 0, s>>>(
         F, trusted, O, bias ? bias_dev : nullptr, N, M, E2, tau, ws, fail));
