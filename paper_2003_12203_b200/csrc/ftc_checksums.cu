@@ -114,10 +114,11 @@ __global__ void k_kernel_checksums(const float* __restrict__ W, int M, int Ckw, 
 // ------------------------------------------------------------------ K4: exact FP64 conv
 // conv_direct (conv.hpp:39-62) at T=double: one thread per output, (k,i,j) ascending,
 // padded taps contribute 0*w exactly like padded_at (:28-37).
-template <typename TI, typename TW>
+template <typename TI, typename TW, int RT>
 __global__ void k_conv_f64_exact(const TI* __restrict__ in, const TW* __restrict__ w,
                                  double* __restrict__ out, int B, int Cin, int H, int Mo, int Ckw,
-                                 int R, int U, int pad, int groups, int E) {
+                                 int Rrt, int U, int pad, int groups, int E) {
+  const int R = RT > 0 ? RT : Rrt;
   const long long total = (long long)B * Mo * E * E;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
@@ -130,17 +131,40 @@ __global__ void k_conv_f64_exact(const TI* __restrict__ in, const TW* __restrict
   const TI* src = in + ((long long)b * Cin + kbase) * H * H;
   const TW* ker = w + (long long)mo * Ckw * R * R;
   double acc = 0.0;
-  for (int k = 0; k < Ckw; ++k)
-    for (int i = 0; i < R; ++i) {
-      const int hh = U * x + i - pad;
-      const bool rok = hh >= 0 && hh < H;
-      for (int j = 0; j < R; ++j) {
-        const int ww = U * y + j - pad;
-        double v = 0.0;
-        if (rok && ww >= 0 && ww < H) v = (double)src[((long long)k * H + hh) * H + ww];
-        acc = dadd(acc, dmul(v, (double)ker[(k * R + i) * R + j]));
+  if constexpr (RT > 0) {
+    // the k x R x R window's loads issue together; the products are added in (k, i, j) order
+    uint32_t vmask = 0;
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = 0; j < RT; ++j) {
+        const int hh = U * x + i - pad, ww = U * y + j - pad;
+        if (hh >= 0 && hh < H && ww >= 0 && ww < H) vmask |= 1u << (i * RT + j);
       }
+    const long long o0 = (long long)(U * x - pad) * H + (U * y - pad);
+    for (int k = 0; k < Ckw; ++k) {
+      double v[RT * RT], wv[RT * RT];
+#pragma unroll
+      for (int t = 0; t < RT * RT; ++t) {
+        v[t] = ((vmask >> t) & 1u) ? (double)src[(long long)k * H * H + o0 + (t / RT) * H + (t % RT)] : 0.0;
+        wv[t] = (double)ker[k * RT * RT + t];
+      }
+#pragma unroll
+      for (int t = 0; t < RT * RT; ++t) acc = dadd(acc, dmul(v[t], wv[t]));
     }
+  } else {
+    for (int k = 0; k < Ckw; ++k)
+      for (int i = 0; i < R; ++i) {
+        const int hh = U * x + i - pad;
+        const bool rok = hh >= 0 && hh < H;
+        for (int j = 0; j < R; ++j) {
+          const int ww = U * y + j - pad;
+          double v = 0.0;
+          if (rok && ww >= 0 && ww < H) v = (double)src[((long long)k * H + hh) * H + ww];
+          acc = dadd(acc, dmul(v, (double)ker[(k * R + i) * R + j]));
+        }
+      }
+  }
   out[idx] = acc;
 }
 
@@ -589,23 +613,30 @@ int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, d
   return FTC_OK;
 }
 
+template <typename TI, typename TW>
+void conv_f64_exact_dispatch(const TI* in, const TW* w, double* out, int B, int Cin, int H, int Mo, int Ckw, int R,
+                             int U, int pad, int groups, int E, int g, cudaStream_t s) {
+  switch (R) {
+    case 1: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 1><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    case 3: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 3><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    case 5: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 5><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    default: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 0><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+  }
+}
+
 int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64, double* out,
                           int B, int Cin, int H, int Mo, int Ckw, int R, int U, int pad,
                           int groups, int E, cudaStream_t s) {
   const long long total = (long long)B * Mo * E * E;
   const int g = blocks_for(total, 128);
   if (in_f64 && w_f64)
-    FTC_LAUNCH(k_conv_f64_exact<double, double><<<g, 128, 0, s>>>((const double*)in, (const double*)w, out, B,
-                                                       Cin, H, Mo, Ckw, R, U, pad, groups, E));
+    conv_f64_exact_dispatch((const double*)in, (const double*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
   else if (in_f64)
-    FTC_LAUNCH(k_conv_f64_exact<double, float><<<g, 128, 0, s>>>((const double*)in, (const float*)w, out, B,
-                                                      Cin, H, Mo, Ckw, R, U, pad, groups, E));
+    conv_f64_exact_dispatch((const double*)in, (const float*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
   else if (w_f64)
-    FTC_LAUNCH(k_conv_f64_exact<float, double><<<g, 128, 0, s>>>((const float*)in, (const double*)w, out, B,
-                                                      Cin, H, Mo, Ckw, R, U, pad, groups, E));
+    conv_f64_exact_dispatch((const float*)in, (const double*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
   else
-    FTC_LAUNCH(k_conv_f64_exact<float, float><<<g, 128, 0, s>>>((const float*)in, (const float*)w, out, B,
-                                                     Cin, H, Mo, Ckw, R, U, pad, groups, E));
+    conv_f64_exact_dispatch((const float*)in, (const float*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
