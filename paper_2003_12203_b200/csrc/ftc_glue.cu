@@ -87,8 +87,12 @@ __device__ __forceinline__ bool ws_arrive(double* ws, long long tick_off, int ti
 // Clean-path Cd1 = sum_n D_n (FP64, any order -- CoC-D is tolerance based; the error
 // path recomputes the exact-order checksums, checksums.hpp:100-107).  Workspace
 // [Cd1][G partial slabs][tickets], zero-filled once: block (x, g) sums image group g at
-// 256 positions (one per thread, 16 loads in flight), and the last group block of each x
+// 256 positions (one per thread, 32 loads in flight), and the last group block of each x
 // folds the slabs into Cd1 (g ascending) and re-arms its ticket.
+#ifndef FTC_CD_UNROLL
+#define FTC_CD_UNROLL 32
+#endif
+constexpr int kCdUnroll = FTC_CD_UNROLL;
 __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, int N, long long per, int NG,
                                                   double* __restrict__ ws, long long tick_off, long long slab_off) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,12 +102,12 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
   if (e < per) {
     double a = 0.0;
     int n = n_lo;
-    for (; n + 16 <= n_hi; n += 16) {  // 16 loads in flight per thread
-      float v[16];
+    for (; n + kCdUnroll <= n_hi; n += kCdUnroll) {  // kCdUnroll loads in flight per thread
+      float v[kCdUnroll];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = __ldcs(D + (long long)(n + u) * per + e);
+      for (int u = 0; u < kCdUnroll; ++u) v[u] = __ldcs(D + (long long)(n + u) * per + e);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) a += (double)v[u];
+      for (int u = 0; u < kCdUnroll; ++u) a += (double)v[u];
     }
     for (; n + 4 <= n_hi; n += 4) {
       float v[4];
