@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       }
     } else {
     const bool pprof = (a.dbg & 64) && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kProdWarps - 1);
-    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+    // per-tile gather state: validity of tap rows i / columns j for this pixel (bit i,
+    // bit 16+j) and the pixel's window origin
+    uint32_t okmask = 0;
+    const float* base = a.D;
+    auto setup = [&](int t) {
       const int pt = a.pt_lo + t % a.npt;
       const long long p = (long long)pt * kBM + r;
       const bool valid = p < a.P;
@@ -421,8 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       const int f = valid ? (int)(p % E2) : 0;
       const int x = f / E, y = f - (f / E) * E;
       const int xb = x * a.U - a.pad, yb = y * a.U - a.pad;
-      // validity of tap rows i / columns j for this pixel (bit i, bit 16+j)
-      uint32_t okmask = 0;
+      okmask = 0;
       if (valid) {
         for (int i = 0; i < R; ++i) {
           if ((unsigned)(xb + i) < (unsigned)H) okmask |= 1u << i;
@@ -432,35 +435,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       // grouped convs: the tile's group's first channel (compile-time 0 otherwise -- any
       // extra live value in this kernel costs the ungrouped hot loops registers)
       const int cg = GROUPED ? (t / a.npt) / a.ntg * a.Ckw : 0;
-      const float* base = NHWC ? a.D + (((long long)n * H + xb) * H + yb) * a.C + cg + hf * 16
-                               : a.D + ((long long)n * a.C + cg) * HH + (long long)xb * H + yb;
-      // software pipeline: the gathers of chunk kc+1 are in flight while chunk kc is
-      // split, waited for and stored into TMEM
-      auto gather = [&](int kc, float (&out)[16]) {
-        if constexpr (NHWC) {
-          const int2 tp = tab_s[kc];
-          const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
-          const float4* src = reinterpret_cast<const float4*>(base + tp.x);
+      base = NHWC ? a.D + (((long long)n * H + xb) * H + yb) * a.C + cg + hf * 16
+                  : a.D + ((long long)n * a.C + cg) * HH + (long long)xb * H + yb;
+    };
+    // software pipeline: the gathers of chunk kc+1 are in flight while chunk kc is split,
+    // waited for and stored into TMEM -- across tiles too (the last chunk of a tile
+    // prefetches the next tile's first chunk; the tile start used to expose a full
+    // gather latency every nkc chunks)
+    auto gather = [&](int kc, float (&out)[16]) {
+      if constexpr (NHWC) {
+        const int2 tp = tab_s[kc];
+        const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+        const float4* src = reinterpret_cast<const float4*>(base + tp.x);
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const float4 f = ok ? __ldg(src + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
-            out[4 * q4 + 0] = f.x;
-            out[4 * q4 + 1] = f.y;
-            out[4 * q4 + 2] = f.z;
-            out[4 * q4 + 3] = f.w;
-          }
-        } else {
-          const int2* tk = tab_s + kc * kBK + hf * 16;
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int2 tp = tk[e];
-            const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
-            out[e] = ok ? __ldg(base + tp.x) : 0.f;
-          }
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 f = ok ? __ldg(src + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          out[4 * q4 + 0] = f.x;
+          out[4 * q4 + 1] = f.y;
+          out[4 * q4 + 2] = f.z;
+          out[4 * q4 + 3] = f.w;
         }
-      };
-      float vn[16];
+      } else {
+        const int2* tk = tab_s + kc * kBK + hf * 16;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int2 tp = tk[e];
+          const bool ok = (okmask & (uint32_t)tp.y) == (uint32_t)tp.y;
+          out[e] = ok ? __ldg(base + tp.x) : 0.f;
+        }
+      }
+    };
+    float vn[16];
+    if ((int)blockIdx.x < ntile_total) {
+      setup(blockIdx.x);
       gather(0, vn);
+    }
+    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
       for (int kc = 0; kc < a.nkc; ++kc, ++g) {
         const uint32_t s = hs, ph = hph;
         hs += 2;
@@ -468,7 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         float v[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = vn[e];
-        if (kc + 1 < a.nkc && !(a.dbg & 1)) gather(kc + 1, vn);
+        if (!(a.dbg & 1)) {
+          if (kc + 1 < a.nkc) {
+            gather(kc + 1, vn);
+          } else if (t + (int)gridDim.x < ntile_total) {
+            setup(t + (int)gridDim.x);
+            gather(0, vn);
+          }
+        }
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
