@@ -84,6 +84,10 @@ constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
 #ifndef FTC_KAS
 #define FTC_KAS 4
 #endif
+#ifndef FTC_EARLY_CORR
+#define FTC_EARLY_CORR 1
+#endif
+constexpr bool kEarlyCorr = FTC_EARLY_CORR;
 constexpr int kAS = FTC_KAS;                 // MODE 2 shared-memory A stages
 constexpr uint32_t kAStageBytes = 128u * 128u;  // 128 pixels x 32 FP32 channels
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
@@ -731,8 +735,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       acc_t sum[HALF];
 #pragma unroll
       for (int jj = 0; jj < HALF; ++jj) sum[jj] = acc_t(0);
+      // the correction accumulator is drained before the last main group (both complete
+      // with the tile's last MMA; same order on every path, so a recomputed plane is
+      // bit-identical to the clean one) and, on the fast path (no hooks, full column
+      // range), released right away -- the next tile's first correction MMA waits for it
+      const bool early_corr = kEarlyCorr && !GROUPED && !a.nfaults && !a.plane_mask &&
+                              nt * BN + half * HALF + HALF <= a.M;
       for (int kc0 = 0; kc0 < a.nkc; kc0 += a.G, ++gc) {
         const uint32_t acc = gc & 1u, aph = (gc >> 1) & 1u;
+        if (kc0 + a.G >= a.nkc) {  // every path adds the correction before the last group
+          mbar_wait_lazy(corrf, tl & 1u);
+          tc_after();
+          const uint32_t cb = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
+#pragma unroll
+          for (int c16 = 0; c16 < HALF / 16; ++c16) {
+            uint32_t v[16];
+            tmem_ld16(cb + (uint32_t)c16 * 16u, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
+          }
+          if (early_corr) {
+            tc_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(corre);
+          }
+        }
         mbar_wait_lazy(accf0 + 8 * acc, aph);
         TC_TRACE(eprof, 6, gc);
         tc_after();
@@ -751,18 +779,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         if (lane == 0) mbar_arrive(acce0 + 8 * acc);
         TC_TRACE(eprof, 7, gc);
       }
-      // the tile's correction accumulator
-      mbar_wait_lazy(corrf, tl & 1u);
-      tc_after();
+      // the tile's correction accumulator (drained above; the slow path below reuses its
+      // columns, so it is released there)
       const uint32_t cbase = tmem + lane_off + corr_col + (uint32_t)(half * HALF);
-#pragma unroll
-      for (int c16 = 0; c16 < HALF / 16; ++c16) {
-        uint32_t v[16];
-        tmem_ld16(cbase + (uint32_t)c16 * 16u, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) sum[c16 * 16 + jj] += (acc_t)__uint_as_float(v[jj]);
-      }
       // tile store + fused FP64 row sums (m order, exact roundings).  Common case: a lean
       // unrolled body after releasing the correction accumulator, so the stores overlap
       // the next tile's MMAs.  Hooks (faults / repair mask) and partial column ranges:
@@ -778,9 +797,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       float* op = a.O + ((long long)n * a.M + m0) * E2 + f;
       const float* bp = a.bias ? a.bias + m0 : nullptr;
       if (mlim == HALF && !a.nfaults && !a.plane_mask) {
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(corre);
+        if (!early_corr) {
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(corre);
+        }
         if (valid) {
           if (bp) {
 #pragma unroll
