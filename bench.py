@@ -389,9 +389,9 @@ def main():
             peak = 148 * 128 * 2 * 1.965e9 / 1e12
             basis = "FP32 SIMT FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz (derived)"
         # DRAM traffic of the conv launches of one step, from the committed ncu --set full
-        # capture of the same workload (profiles/r01c_traffic.json; AlexNet only)
+        # capture of the same workload (profiles/r01d_traffic.json; AlexNet only)
         traffic = None
-        tj = os.path.join(ROOT, "profiles", "r01c_traffic.json")
+        tj = os.path.join(ROOT, "profiles", "r01d_traffic.json")
         if args.workload == "alexnet" and os.path.exists(tj):
             traffic = json.load(open(tj))["conv_dram_bytes_per_step"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
