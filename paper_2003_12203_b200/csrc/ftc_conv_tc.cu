@@ -9,7 +9,7 @@
 // lo = RN_tf32(v - hi); each K step issues lo*Bhi + hi*Blo + hi*Bhi into one FP32
 // TMEM accumulator (the dropped lo*lo term is 2^-22 relative).
 //
-// Warp roles (persistent CTA per SM, 608 threads):
+// Warp roles (persistent CTA per SM, 640 threads):
 //   warps 0-7   A producers (two per TMEM lane quarter): gather the im2col row of their
 //               pixel straight from D (L1/L2-resident halo), split hi/lo and tcgen05.st
 //               it into a TMEM half-stage (warps 0-3: K columns 0-15 of a chunk, 4-7:
