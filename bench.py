@@ -3,21 +3,31 @@
 "ABFT-protected conv images/s, checksum overhead %, % of roofline").
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload alexnet|config1]
+                  [--workload vgg19|alexnet|resnet18|yolov2|config1] [--policy detection|all-families]
+                  [--no-extras] [--no-cpu-baseline]
 
-One step = one protected forward pass over one batch of seeded synthetic input
-(no dataset): for `alexnet` (BASELINE configs[1], the default) the
-5-layer AlexNet-style stack at batch 128 with every conv ABFT-protected; for
-`config1` the single 64->64 3x3 layer at batch 16.  Every timing is taken with CUDA
-events on the launching stream; L2 is flushed (256 MiB write) before every timed
-step.  Multi-GPU (torchrun) runs one shard per rank (weak scaling: each rank owns a
-full batch), gathers the per-shard verdict records with NCCL and reports the MAX
-step time over ranks.  Rank 0 prints one JSON line.
+One step = one protected forward over one batch of seeded synthetic input (no
+dataset).  The headline workload is the largest single-GPU BASELINE
+config, the VGG-19 conv trunk at global batch 64 (configs[2], 2.50 TFLOP per step);
+AlexNet b128, ResNet-18 b256, YOLOv2 b64 and the single config-1 layer are reported as
+`extra_workloads` records of the same run.  Every timing is taken with CUDA events on
+the launching stream, after an L2 flush (256 MiB write) before every step.
+
+Multi-GPU (torchrun, one rank per GPU): the config's GLOBAL batch is sharded
+(dist.shard_range, strong scaling); each rank runs its own ABFT on its shard with
+shard-calibrated tau_L, and the step ends with the NCCL all-gather of the per-layer
+verdict records (the only collective of the path), inside the timed region.  The
+step time is the max over ranks; rank 0 prints ONE JSON line.
+
+`--impl reference` times the reference's own CPU path (oracle/_ref: the unmodified
+reference headers' run_protected_layer<float>, make_default_plan, ConvImpl::direct)
+on the host cores, on the same workload (bounded per-step sample, see `cpu_sample`).
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -31,15 +41,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ABFT-protected conv images/s, checksum overhead %, % of roofline"
+WORKLOADS = {"config1": "config1_conv_n16_c64_h56_m64_r3", "alexnet": "alexnet5_conv_stack_b128_fp32",
+             "vgg19": "vgg19_conv_trunk_b64_fp32", "resnet18": "resnet18_convs_b256_fp32",
+             "yolov2": "yolov2_darknet19_convs_b64_fp32"}
+# 128x128x8 TF32 tcgen05.mma = 64.1 cycles (tools/ubench_tmem.cu):
+# useful FP32 FLOP per SM-cycle of a 3xTF32 conv
+TF32_FLOP_PER_SM_CYCLE_3X = 2 * 128 * 128 * 8 / 64.1 / 3
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return p, "measured"
+            return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -103,28 +128,31 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- workloads
 class Config1:
     """BASELINE configs[0]: one 64->64 3x3 conv layer, N=16, H=56, FP32, all four schemes."""
-    name = "config1_conv_n16_c64_h56_m64_r3"
+    name = "config1"
 
-    def __init__(self, seed: int, dev):
+    def __init__(self, dev, shard=None, **_):
         import torch
         import paper_2003_12203_b200 as F
         from paper_2003_12203_b200 import synth
         self.F = F
-        D, W = synth.config1(seed)
-        self.batch = 16
+        D, W = synth.config1(12345)
+        lo, hi = shard if shard is not None else (0, 16)
+        D = np.ascontiguousarray(D[lo:hi])
+        self.batch = hi - lo
+        self.global_batch = 16
+        self.lo = lo
         self.p = F.ConvParams(pad=1)
-        self.layer = F.ProtectedConv(W, None, self.p, 16, 56)
+        self.layer = F.ProtectedConv(W, None, self.p, self.batch, 56)
+        self.taus = {"conv": 1e-3}
         self.plan = F.LayerPlan(rc_enabled=True, clc_enabled=True, tau=1e-3)
         self.D = torch.from_numpy(D).to(dev)
         self.O = torch.empty(self.layer.out_shape, dtype=torch.float32, device=dev)
         self.D_host = torch.from_numpy(D).pin_memory()
         self.O_host = torch.empty(self.layer.out_shape, dtype=torch.float32).pin_memory()
-        self.flops = 2.0 * 16 * 64 * 56 * 56 * 64 * 9
+        self.flops = 2.0 * self.batch * 64 * 56 * 56 * 64 * 9
         self.layers = [self.layer]
         self.in_bytes = D.nbytes
         self.out_bytes = self.O_host.numel() * 4
-        self.D_np = D
-        self.W_np = W
 
     def launch(self):
         self.layer.launch(self.D, self.O, self.plan)
@@ -141,111 +169,212 @@ class Config1:
         _, rep = self.layer.protected_host(Dn, self.plan, O=On)
         return [rep]
 
+    def close(self):
+        self.layer.close()
 
-def build_workload(name: str, seed: int, dev):
+
+def build_workload(name: str, dev, policy: str, shard=None):
     if name == "config1":
-        return Config1(seed, dev)
+        return Config1(dev, shard)
     from paper_2003_12203_b200 import nets
-    return nets.BenchNet(name, seed, dev)
+    return nets.BenchNet(name, dev, policy=policy, shard=shard)
+
+
+def global_batch_of(name: str) -> int:
+    if name == "config1":
+        return 16
+    from paper_2003_12203_b200 import nets
+    return nets.NETS[name]()["batch"]
+
+
+# ----------------------------------------------------------------------------- cuDNN anchor
+def cudnn_forward_fn(wl, dev):
+    """The same conv stack (same weights, glue, shard batch) through torch/cuDNN in FP32
+    with TF32 disabled: the external library anchor; unprotected."""
+    import torch
+    import torch.nn.functional as TF
+    from paper_2003_12203_b200 import nets
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.benchmark = True
+    if not hasattr(wl, "pn"):  # config1
+        W = torch.from_numpy(wl.layer._W).to(dev)
+        return lambda: TF.conv2d(wl.D, W, None, 1, 1)
+    pn = wl.pn
+    Ws = {k: (torch.from_numpy(w).to(dev), None if b is None else torch.from_numpy(b).to(dev))
+          for k, (w, b) in pn.weights.items()}
+    ops = pn.net["ops"]
+    x0 = pn.buf["x"]
+
+    def act(t, a):
+        if a == "relu":
+            return TF.relu(t)
+        if a == "leaky":
+            return TF.leaky_relu(t, 0.1)
+        return t
+
+    def run():
+        t = {"x": x0}
+        for op in ops:
+            if isinstance(op, nets.Conv):
+                W, b = Ws[op.dst]
+                t[op.dst] = TF.conv2d(t[op.src], W, b, op.stride, op.pad)
+            elif isinstance(op, nets.ActPool):
+                y = act(t[op.src], op.act)
+                if op.k > 1 or op.s > 1:
+                    y = TF.max_pool2d(y, op.k, op.s, op.p)
+                t[op.dst] = y
+            elif isinstance(op, nets.AddAct):
+                t[op.dst] = act(t[op.a] + t[op.b], op.act)
+            elif isinstance(op, nets.PadCrop):
+                t[op.dst] = TF.pad(t[op.src], (op.lo, op.hi, op.lo, op.hi))
+        return t
+    return run
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def _ref_worker(args):
-    """One process: the reference's shipped CPU path on a bounded sample."""
-    workload, seed, images = args
+def _np_act_pool(x, act, k, s, p):
+    if act == "relu":
+        x = np.maximum(x, 0)
+    elif act == "leaky":
+        x = np.where(x > 0, x, np.float32(0.1) * x)
+    if k == 1 and s == 1 and p == 0:
+        return x.astype(np.float32)
+    N, Cc, H, _ = x.shape
+    Ho = (H + 2 * p - k) // s + 1
+    xp = np.full((N, Cc, H + 2 * p, H + 2 * p), -np.inf, np.float32)
+    xp[:, :, p:p + H, p:p + H] = x
+    out = np.full((N, Cc, Ho, Ho), -np.inf, np.float32)
+    for i in range(k):
+        for j in range(k):
+            out = np.maximum(out, xp[:, :, i:i + s * Ho:s, j:j + s * Ho:s][:, :, :Ho, :Ho])
+    return out
+
+
+def cpu_tasks(workload: str):
+    """The per-image CPU work of one step, as independent layer tasks.
+
+    Every protected conv of the net on ONE image (N=1) through the reference's
+    run_protected_layer<float> (make_default_plan, tau 1e-4, ConvImpl::direct),
+    followed by its act/pool glue in numpy (the reference has no glue ops).  Inputs
+    are seeded synthetic activations of each layer's shape (N(0,1) / U(0,1) for the
+    first layer as the config states, ReLU'd N(0,1) after it): the direct conv's cost
+    does not depend on the values.  Config 1: the 16 images of the batch, one task
+    each."""
+    from paper_2003_12203_b200 import nets, synth
+    if workload == "config1":
+        return [("config1", n) for n in range(16)]
+    net = nets.NETS[workload]()
+    _, convs = nets.shapes(net)
+    cost = [op.M * E * E * Cin * op.R * op.R for op, Cin, H, E in convs]
+    order = sorted(range(len(convs)), key=lambda li: -cost[li])  # longest first
+    return [(workload, li) for li in order]
+
+
+def _cpu_task(args):
+    """One task on one host core -> CPU-seconds (the reference's own CPU path)."""
+    workload, idx = args
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_py as O
-    from paper_2003_12203_b200 import synth
-    t0 = time.perf_counter()
+    from paper_2003_12203_b200 import nets, synth
     if workload == "config1":
-        D, W = synth.config1(seed)
-        d = O.dims(images, 64, 56, 64, 3, 1, 1)
-        O.ref_protected_layer_f32(d, D[:images], W, None, tau=1e-4)
+        D, W = synth.config1(12345)
+        d = O.dims(1, 64, 56, 64, 3, 1, 1)
+        t0 = time.perf_counter()
+        O.ref_protected_layer_f32(d, D[idx:idx + 1], W, None, tau=1e-4)
+        return time.perf_counter() - t0
+    net = nets.NETS[workload]()
+    _, convs = nets.shapes(net)
+    op, Cin, H, E = convs[idx]
+    W, b = nets.net_weights(net, 11)[op.dst]
+    if idx == 0:
+        x = nets.net_input(net, 1, 77)
     else:
-        from paper_2003_12203_b200 import nets
-        nets.reference_forward(workload, seed, images)
+        x = np.maximum(synth.normal((1, Cin, H, H), 1.0, 77 + idx), 0)
+    d = O.dims(1, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias)
+    t0 = time.perf_counter()
+    _, out = O.ref_protected_layer_f32(d, x, W, b, tau=1e-4)
+    # the layer's consumer glue (act + pool) as a numpy restatement
+    nxt = [o for o in net["ops"] if isinstance(o, nets.ActPool) and o.src == op.dst]
+    for g in nxt:
+        _np_act_pool(out, g.act, g.k, g.s, g.p)
     return time.perf_counter() - t0
 
 
-def cpu_reference(workload: str, images_per_proc: int, procs: int, seed: int = 7):
+def cpu_sample(workload: str, procs: int):
+    """One step of the reference CPU arm: the workload's tasks spread over `procs`
+    concurrent single-threaded processes (longest first).  Returns (images/s,
+    wall seconds, CPU-seconds per image).  images/s = procs / CPU-seconds per image: the
+    throughput of `procs` cores each running whole images, with the per-layer costs
+    measured under full-host concurrency."""
     import multiprocessing as mp
+    tasks = cpu_tasks(workload)
     ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        ts = pool.map(_ref_worker, [(workload, seed + i, images_per_proc) for i in range(procs)])
-    t = max(ts)
-    return images_per_proc * procs / t, t
+    t0 = time.perf_counter()
+    with ctx.Pool(min(procs, len(tasks))) as pool:
+        secs = pool.map(_cpu_task, tasks, chunksize=1)
+    wall = time.perf_counter() - t0
+    if workload == "config1":
+        per_image = sum(secs) / 16.0
+    else:
+        per_image = sum(secs)
+    return procs / per_image, wall, per_image
 
 
-def ref_sample_size(workload: str) -> int:
-    return 2 if workload == "config1" else 1
+def cpu_sample_text(workload, procs):
+    if workload == "config1":
+        return (f"the 16 config-1 images, one per task (N=1 each), over {procs} single-threaded processes; "
+                "reference run_protected_layer<float> (make_default_plan, tau 1e-4, ConvImpl::direct) via "
+                "oracle/_ref; images/s = cores / CPU-seconds per image")
+    return (f"one image through every protected conv of the net (each layer a task, N=1, seeded synthetic "
+            f"activations of the layer's shape) + numpy act/pool glue, tasks spread over {procs} single-threaded "
+            "processes; reference run_protected_layer<float> (make_default_plan, tau 1e-4, ConvImpl::direct) via "
+            "oracle/_ref; images/s = cores / CPU-seconds per image")
 
 
-# ----------------------------------------------------------------------------- main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=os.environ.get("FTC_BENCH_WORKLOAD", "alexnet"))
-    ap.add_argument("--engine", default="tc", choices=["tc", "simt"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    cores = os.cpu_count() or 1
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        per = ref_sample_size(args.workload)
-        procs = cores
-        vals = []
-        for _ in range(args.warmup if args.warmup < 1 else 1):
-            pass
-        t_all = []
-        for _ in range(args.steps):
-            v, t = cpu_reference(args.workload, per, procs)
-            vals.append(v)
-            t_all.append(t)
-        value = statistics.median(vals)
-        sample = (f"{per} image(s) per process x {procs} processes per step through the reference's "
-                  f"run_protected_layer<float> (make_default_plan, ConvImpl::direct), oracle/_ref")
-        line = {
-            "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * statistics.median(t_all), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(args.workload), "global_batch": per * procs},
-            "cpu_baseline": {"value": value, "unit": "images/s", "cores": procs, "kind": "reference",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line))
+def run_reference(args, rank):
+    if rank != 0:
         return
+    procs = os.cpu_count() or 1
+    wl = args.workload
+    for _ in range(args.warmup):
+        cpu_sample(wl, procs)
+    vals, walls, per = [], [], []
+    for _ in range(args.steps):
+        v, w, p = cpu_sample(wl, procs)
+        vals.append(v)
+        walls.append(w)
+        per.append(p)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(walls), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
+        "config": {"workload": WORKLOADS[wl], "global_batch": global_batch_of(wl),
+                   "cpu_seconds_per_image": statistics.median(per)},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": procs, "kind": "reference",
+                         "cpu_model": cpu_model(), "sample": cpu_sample_text(wl, procs)},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
 
+
+# ----------------------------------------------------------------------------- GPU measurement
+def measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, headline=True):
+    """Protected steps, conv-kernel roofline pass, unprotected steps, e2e, cuDNN anchor,
+    detection campaigns.  Returns the per-rank numbers (times are reduced by the caller)."""
+    import ctypes as C
     import torch
     import torch.distributed as dist
-    if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    import paper_2003_12203_b200 as F
-    from paper_2003_12203_b200 import _abi
-    F.set_conv_engine(args.engine)
-    lib = _abi.lib()
-    peaks, peak_kind = load_peaks()
-
-    wl = build_workload(args.workload, 1000 + rank, dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    from paper_2003_12203_b200 import dist as ftc_dist
     stream = torch.cuda.current_stream()
+    steps = args.steps if headline else max(3, min(args.steps, 10))
+    warm = args.warmup
 
-    def timed(fn, steps, sync_each=True):
+    def timed(fn, k):
         tot = 0.0
-        for _ in range(steps):
+        for _ in range(k):
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -254,32 +383,25 @@ def main():
             e1.record(stream)
             e1.synchronize()
             tot += e0.elapsed_time(e1)
-        return tot
+        return tot / k
 
-    # warm-up (protected + unprotected + e2e)
-    for _ in range(args.warmup):
+    for _ in range(warm):
         wl.launch(); wl.finish(); wl.unprotected(); wl.e2e()
-    if hasattr(wl, "e2e_stream"):
+    if hasattr(wl, "e2e_stream") and headline:
         wl.e2e_stream(2)
     torch.cuda.synchronize()
 
-    # ---- protected, inputs resident in HBM: device time of the clean path (no per-kernel
-    # instrumentation here: event records between launches would cut the programmatic
-    # dependent launches; the conv kernel times come from a second pass below)
-    from paper_2003_12203_b200 import dist as ftc_dist
-    reports = []
-    verdict_tables = []
+    # ---- protected steps, inputs resident: launch every layer, read the verdicts, and
+    # (N>1) all-gather the per-layer verdict records -- all inside the timed region
+    tables = []
     l0 = lib.ftc_kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-
-    def prot():
-        wl.launch()
     tot = 0.0
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.fill_(1.0)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -287,161 +409,245 @@ def main():
         torch.cuda.nvtx.range_push("timed_step")  # ncu --nvtx --nvtx-include timed_step/
         wl.launch()
         torch.cuda.nvtx.range_pop()
-        e1.record(stream)
         reps = wl.finish()
-        reports.append(reps)
-        if world > 1:
-            # per-forward verdict exchange: the only collective of the ABFT path
-            verdict_tables.append(ftc_dist.gather_verdicts(reps, dev))
+        tables.append(ftc_dist.gather_verdicts(reps, dev, getattr(wl, "lo", 0)))
+        e1.record(stream)
         e1.synchronize()
         tot += e0.elapsed_time(e1)
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = lib.ftc_kernel_launches() - l0
-    t_prot = tot / args.steps
+    t_prot = tot / steps
 
-    # ---- roofline pass: the same K protected steps with CUDA events bracketing every
-    # conv launch on its stream (ftc_layer_set_timing)
+    # ---- roofline pass: the same protected steps with CUDA events around every conv
+    # launch on its stream (ftc_layer_set_timing)
     for L in wl.layers:
         lib.ftc_layer_set_timing(L.h, 1)
         lib.ftc_layer_kernel_time(L.h, None, None, 1)
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.fill_(1.0)
         wl.launch()
         wl.finish()
     torch.cuda.synchronize()
-    conv_ms = []
+    conv_ms, conv_n = 0.0, 1
     for L in wl.layers:
-        import ctypes as C
         ms = C.c_double(); n = C.c_int32()
         lib.ftc_layer_kernel_time(L.h, C.byref(ms), C.byref(n), 1)
-        conv_ms.append((ms.value, n.value))
+        conv_ms += ms.value
+        conv_n = max(conv_n, n.value)
         lib.ftc_layer_set_timing(L.h, 0)
+    conv_ms /= conv_n
 
-    # ---- unprotected conv stack (same kernels, no ABFT) for the overhead
-    t_unprot = timed(wl.unprotected, args.steps) / args.steps
+    t_unprot = timed(wl.unprotected, steps)
 
-    # ---- e2e through the C-ABI host entry points (H2D of D, D2H of O inside the region)
-    t_e2e = timed(wl.e2e, max(3, args.steps // 2)) / max(3, args.steps // 2)
+    # ---- e2e through the host API (H2D of the step's input, D2H of its output inside
+    # the region; pinned host buffers)
+    ne = max(3, steps // 2)
+    t_e2e = timed(wl.e2e, ne)
     t_e2e_serial = t_e2e
-    if hasattr(wl, "e2e_stream"):
-        # the same host API with batch k+1's H2D overlapped with batch k's forward
-        # (HostPipeline): every batch still crosses H2D and its result D2H inside the
-        # region, and the L2 flush runs on the compute stream ahead of every batch
-        wl.e2e_stream(max(1, args.warmup), before_step=lambda: flush.fill_(1.0))  # untimed warm-up
+    e2e_mode = "serial"
+    if hasattr(wl, "e2e_stream") and headline:
+        wl.e2e_stream(max(1, warm), before_step=lambda: flush.fill_(1.0))
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        wl.e2e_stream(args.steps, before_step=lambda: flush.fill_(1.0), start_event=e0)
+        wl.e2e_stream(steps, before_step=lambda: flush.fill_(1.0), start_event=e0)
         e1.record(stream)
         e1.synchronize()
-        t_e2e = e0.elapsed_time(e1) / args.steps
+        t_e2e = e0.elapsed_time(e1) / steps
+        e2e_mode = "pipelined: nets.HostPipeline over two nets, batch k+1's H2D and launch under batch k"
 
-    # ---- faulted forwards (BASELINE: one seeded output bit flip per layer): detection,
-    # localisation, repair and downstream replay on the device, timed end to end
-    faulted = None
-    if hasattr(wl, "faulted"):
-        runs, stages, t_f, repaired_ok, repaired_runs = 3, {}, 0.0, True, 0
-        for r in range(runs):
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            reps_f, same = wl.faulted(r)
-            torch.cuda.synchronize()
-            t_f += time.perf_counter() - t0
-            for rep in reps_f:
-                stages[rep.stage] = stages.get(rep.stage, 0) + 1
-            # a sub-threshold (undetected) or discarded flip stays in the output by design;
-            # when every layer repaired its flip the net output must be the fault-free one
-            if all(rep.stage in ("coc", "rc", "clc", "fc", "recompute") for rep in reps_f):
-                repaired_runs += 1
-                repaired_ok = repaired_ok and same
-        faulted = {"ms_per_forward": 1e3 * t_f / runs, "runs": runs, "flips_per_forward": len(wl.layers),
-                   "stages": stages, "fully_repaired_runs": repaired_runs,
-                   "fully_repaired_output_equals_fault_free": repaired_ok,
-                   "timing": "host wall clock around forward (launch + verdicts + repairs + replays)"}
+    # ---- cuDNN FP32 anchor (TF32 off), same stack and shard, unprotected
+    t_cudnn = None
+    try:
+        fn = cudnn_forward_fn(wl, dev)
+        for _ in range(warm):
+            fn()
+        t_cudnn = timed(fn, steps)
+    except Exception as e:  # pragma: no cover
+        t_cudnn = None
+        print(f"cudnn anchor failed: {e}", file=sys.stderr)
 
-    # max over ranks
-    tt = torch.tensor([t_prot, t_unprot, t_e2e, t_e2e_serial], dtype=torch.float64, device=dev)
-    detected = sum(1 for reps in reports for r in reps if r.detected)
+    # ---- detection campaigns under both tau policies (faulted forwards)
+    campaigns = None
+    if hasattr(wl, "campaign") and args.campaign_runs > 0:
+        campaigns = {}
+        runs = args.campaign_runs if headline else max(2, args.campaign_runs // 2)
+        base_policy = wl.policy
+        from paper_2003_12203_b200 import nets
+        for pol in nets.TAU_POLICIES:
+            wl.set_policy(pol)
+            campaigns[pol] = wl.campaign(runs)
+        wl.set_policy(base_policy)
+
+    detected = sum(ftc_dist.summarize(tab)["detected"] for tab in tables)
+    return {"t_prot": t_prot, "t_unprot": t_unprot, "t_e2e": t_e2e, "t_e2e_serial": t_e2e_serial,
+            "conv_ms": conv_ms, "t_cudnn": t_cudnn, "clocks": clocks, "launches": launches, "steps": steps,
+            "campaigns": campaigns, "detected": detected, "e2e_mode": e2e_mode,
+            "verdict_table_last": tables[-1] if tables else None}
+
+
+def reduce_max(vals, dev, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v if v is not None else -1.0 for v in vals], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        detected = sum(ftc_dist.summarize(tab)["detected"] for tab in verdict_tables)
-    t_prot, t_unprot, t_e2e, t_e2e_serial = tt.tolist()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [None if v < 0 else v for v in t.tolist()]
+
+
+def record(name, wl, r, world, peaks, peak_kind, global_batch):
+    """JSON record of one workload from the reduced per-rank numbers."""
+    t_prot, t_unprot, t_e2e, t_e2e_serial, conv_ms, t_cudnn = (
+        r["t_prot"], r["t_unprot"], r["t_e2e"], r["t_e2e_serial"], r["conv_ms"], r["t_cudnn"])
+    flops_global = wl.flops * (global_batch / wl.batch)  # every shard does its share
+    achieved = wl.flops / (conv_ms / 1e3) / 1e12  # per rank: the dominant kernel's rate
+    peak = peaks["bf16_tflops"] / 2.0 / 3.0
+    sm_mhz = (r["clocks"] or {}).get("sm_mhz") or 1965.0
+    clock_ceiling = TF32_FLOP_PER_SM_CYCLE_3X * 148 * sm_mhz * 1e6 / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None,
+            "kernel": "k_conv_tc (tcgen05 3xTF32 implicit GEMM), all conv launches of one step",
+            "kernel_ms_per_step": conv_ms,
+            "peak_basis": (f"3xTF32 useful-FP32 ceiling = {peak_kind} bf16 burst {peaks['bf16_tflops']} TF/s / 2 (TF32) "
+                           "/ 3 (passes)"),
+            "clock_ceiling": {"value": clock_ceiling, "frac": achieved / clock_ceiling,
+                              "basis": (f"64.1 cycles per 128x128x8 TF32 MMA (tools/ubench_tmem.cu) x 148 SMs x "
+                                        f"{sm_mhz:.0f} MHz (median SM clock in the timed region) / 3")},
+            "kernel_timing": "CUDA events around each conv launch on its stream, second pass of the protected steps",
+            "flops_per_step_per_gpu": wl.flops, "algorithmic_unit": "2*N*M*E^2*C*R^2 FLOP per conv"}
+    tr = os.path.join(ROOT, "profiles", f"r02_traffic_{name}.json")
+    if os.path.exists(tr) and world == 1:
+        tj = json.load(open(tr))
+        roof["traffic"] = tj.get("conv_dram_bytes_per_step")
+        roof["traffic_unit"] = "DRAM bytes read+written by the conv launches of one step (ncu --set full)"
+        roof["traffic_algorithmic_bytes"] = tj.get("conv_algorithmic_bytes_per_step")
+    out = {"value": global_batch / (t_prot / 1e3), "ms_per_step": t_prot,
+           "abft_overhead_pct": 100.0 * (t_prot - t_unprot) / t_unprot, "ms_per_step_unprotected": t_unprot,
+           "roofline": roof,
+           "e2e": {"value": global_batch / (t_e2e / 1e3), "unit": "images/s",
+                   "h2d_bytes_per_step": wl.in_bytes * world, "d2h_bytes_per_step": wl.out_bytes * world,
+                   "mode": r["e2e_mode"], "serial_value": global_batch / (t_e2e_serial / 1e3)},
+           "detections_in_timed_region": r["detected"], "flops_per_step": flops_global}
+    if t_cudnn is not None:
+        out["cudnn_fp32_anchor"] = {
+            "ms_per_step": t_cudnn, "images_s": global_batch / (t_cudnn / 1e3),
+            "what": "torch F.conv2d (cuDNN, FP32, TF32 off, benchmark mode) + the same glue, unprotected",
+            "protected_speedup_vs_cudnn": t_cudnn / t_prot, "unprotected_speedup_vs_cudnn": t_cudnn / t_unprot}
+    if r.get("campaigns"):
+        out["detection"] = r["campaigns"]
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=os.environ.get("FTC_BENCH_WORKLOAD", "vgg19"), choices=sorted(WORKLOADS))
+    ap.add_argument("--policy", default="detection", choices=["detection", "all-families"])
+    ap.add_argument("--engine", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--campaign-runs", type=int, default=8)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import _abi
+    from paper_2003_12203_b200 import dist as ftc_dist
+    F.set_conv_engine(args.engine)
+    lib = _abi.lib()
+    peaks, peak_kind = load_peaks()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one(name, headline):
+        gb = global_batch_of(name)
+        shard = ftc_dist.shard_range(gb, world, rank)
+        wl = build_workload(name, dev, args.policy, shard)
+        r = measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, headline)
+        keys = ["t_prot", "t_unprot", "t_e2e", "t_e2e_serial", "conv_ms", "t_cudnn"]
+        red = reduce_max([r[k] for k in keys], dev, world)
+        r.update(dict(zip(keys, red)))
+        r["detected"] = int(r["detected"])  # already job-wide: summed over the gathered tables
+        rec = record(name, wl, r, world, peaks, peak_kind, gb)
+        rec["config"] = {"workload": WORKLOADS[name], "global_batch": gb, "per_gpu_batch": wl.batch,
+                         "shard": list(shard), "parallelism": f"dp{world} (batch-sharded)",
+                         "l2": "flushed (256 MiB write) before every step",
+                         "plan": f"rc+clc on, per-layer tau ({args.policy} policy, calibrated per shard)",
+                         "tau_per_layer": getattr(wl, "taus", None)}
+        rec["launches"] = r["launches"]
+        rec["steps"] = r["steps"]
+        rec["clocks"] = r["clocks"]
+        wl.close()
+        torch.cuda.synchronize()
+        return rec
+
+    head = one(args.workload, True)
+    extras = {}
+    if not args.no_extras:
+        for name in ["alexnet", "resnet18", "yolov2", "config1"]:
+            if name == args.workload:
+                continue
+            if world > 1 and global_batch_of(name) < world:
+                continue
+            try:
+                rec = one(name, False)
+                for k in ("clocks",):
+                    rec.pop(k, None)
+                extras[name] = rec
+            except Exception as e:  # pragma: no cover
+                extras[name] = {"error": str(e)}
 
     if rank == 0:
-        images = wl.batch * world
-        value = images / (t_prot / 1e3)
-        overhead = 100.0 * (t_prot - t_unprot) / t_unprot
-        # dominant kernel roofline: the conv (tensor-bound); 3xTF32 issues 3 MMAs per
-        # useful FP32 MAC, so its ceiling is the TF32 dense peak / 3, where TF32 =
-        # measured bf16 / 2 (datasheet ratio)
-        tot_ms = sum(m for m, _ in conv_ms)
-        tot_n = max(1, max(n for _, n in conv_ms))
-        conv_avg_ms = tot_ms / tot_n  # per protected forward
-        achieved = wl.flops / (conv_avg_ms / 1e3) / 1e12
-        if args.engine == "tc":
-            peak = peaks["bf16_tflops"] / 2.0 / 3.0
-            basis = (f"3xTF32 useful-FP32 ceiling = {peak_kind} bf16 burst {peaks['bf16_tflops']} TF/s "
-                     "/ 2 (TF32) / 3 (passes)")
-        else:
-            peak = 148 * 128 * 2 * 1.965e9 / 1e12
-            basis = "FP32 SIMT FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz (derived)"
-        # DRAM traffic of the conv launches of one step, from the committed ncu --set full
-        # capture of the same workload (profiles/r01d_traffic.json; AlexNet only)
-        traffic = None
-        tj = os.path.join(ROOT, "profiles", "r01d_traffic.json")
-        if args.workload == "alexnet" and os.path.exists(tj):
-            traffic = json.load(open(tj))["conv_dram_bytes_per_step"]
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step (5 conv launches)",
-                "kernel": "conv (sum over layers per step)",
-                "kernel_ms_per_step": conv_avg_ms, "peak_basis": basis,
-                "kernel_timing": "CUDA events around each conv launch, second pass of K protected steps",
-                "flops_per_step": wl.flops}
         cpu = None
         if not args.no_cpu_baseline and world == 1:
+            procs = os.cpu_count() or 1
             try:
-                per = ref_sample_size(args.workload)
-                v, t = cpu_reference(args.workload, per, cores)
-                cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "reference",
-                       "sample": f"{per} image(s) x {cores} processes, reference run_protected_layer<float> "
-                                 f"(default plan) via oracle/_ref, {t:.1f} s"}
+                v, wall, per = cpu_sample(args.workload, procs)
+                cpu = {"value": v, "unit": "images/s", "cores": procs, "kind": "reference",
+                       "cpu_model": cpu_model(), "cpu_seconds_per_image": per,
+                       "sample": cpu_sample_text(args.workload, procs) + f"; one sample, {wall:.1f} s wall"}
             except Exception as e:  # pragma: no cover
-                cpu = {"value": None, "unit": "images/s", "cores": cores, "kind": "reference",
+                cpu = {"value": None, "unit": "images/s", "cores": procs, "kind": "reference",
                        "sample": f"unavailable: {e}"}
         line = {
-            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_prot,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded; no dataset)",
-            "config": {"workload": workload_name(args.workload), "global_batch": images,
-                       "per_gpu_batch": wl.batch, "engine": args.engine,
-                       "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every step",
-                       "plan": "rc+clc on, per-layer tau",
-                       "tau_per_layer": getattr(wl, "taus", None)},
-            "abft_overhead_pct": overhead, "ms_per_step_unprotected": t_unprot,
-            "roofline": roof, "cpu_baseline": cpu,
-            "e2e": {"value": images / (t_e2e / 1e3), "unit": "images/s",
-                    "h2d_bytes_per_step": wl.in_bytes, "d2h_bytes_per_step": wl.out_bytes,
-                    "mode": ("pipelined: nets.HostPipeline over two nets, batch k+1's H2D and launch under batch k"
-                             if hasattr(wl, "e2e_stream") else "serial"),
-                    "serial_value": images / (t_e2e_serial / 1e3)},
-            "gpu_launches": int(launches), "launches_per_step": launches / args.steps,
-            "clocks": clocks, "detections_in_timed_region": detected,
-            "faulted_forward": faulted,
+            "metric": METRIC, "value": head["value"], "unit": "images/s", "n_gpus": world,
+            "steps": head["steps"], "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded; no dataset)",
+            "config": head["config"],
+            "abft_overhead_pct": head["abft_overhead_pct"], "ms_per_step_unprotected": head["ms_per_step_unprotected"],
+            "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head["e2e"],
+            "gpu_launches": int(head["launches"]), "launches_per_step": head["launches"] / head["steps"],
+            "clocks": head["clocks"], "detections_in_timed_region": head["detections_in_timed_region"],
+            "timed_step": ("launch every layer's clean path, read the per-layer verdict records, all-gather them "
+                           "across ranks (NCCL; a no-op at N=1)"),
         }
+        for k in ("cudnn_fp32_anchor", "detection"):
+            if k in head:
+                line[k] = head[k]
+        line["extra_workloads"] = extras
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def workload_name(w: str) -> str:
-    return {"config1": Config1.name, "alexnet": "alexnet5_conv_stack_b128_fp32",
-            "vgg19": "vgg19_conv_trunk_b64_fp32", "resnet18": "resnet18_convs_b256_fp32",
-            "yolov2": "yolov2_darknet19_convs_b64_fp32"}.get(w, w)
 
 
 if __name__ == "__main__":

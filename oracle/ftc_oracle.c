@@ -849,6 +849,12 @@ static void report_finish(or_report* rep, const outcome* oc, int stage) {
 int or_protected_layer(const or_dims* d, const double* D, const double* W_golden, const double* bias,
                        const or_plan* plan, const double* O_conv, const or_pre_fault* pre, int n_pre,
                        or_report* rep, double* O_out) {
+  return or_protected_layer_seam(d, D, W_golden, bias, plan, O_conv, NULL, pre, n_pre, rep, O_out);
+}
+
+int or_protected_layer_seam(const or_dims* d, const double* D, const double* W_golden, const double* bias,
+                            const or_plan* plan, const double* O_conv, const double* O_recompute,
+                            const or_pre_fault* pre, int n_pre, or_report* rep, double* O_out) {
   memset(rep, 0, sizeof *rep);
   layer_state L;
   int st = state_init(&L, d, D, W_golden, bias, plan->tau);
@@ -947,8 +953,11 @@ int or_protected_layer(const or_dims* d, const double* D, const double* W_golden
     double* co5 = malloc(sizeof(double) * L.E2);
     double* so5 = malloc(sizeof(double) * L.E2);
     for (int attempt = 0; attempt < 2; ++attempt) {
-      conv_f64(d->N, d->C, d->H, d->M, d->C / d->groups, d->R, d->stride, d->pad, d->groups, L.E,
-               L.D, L.W, d->bias ? bias : NULL, L.O);
+      if (O_recompute)
+        memcpy(L.O, O_recompute, sizeof(double) * nO);
+      else
+        conv_f64(d->N, d->C, d->H, d->M, d->C / d->groups, d->R, d->stride, d->pad, d->groups, L.E,
+                 L.D, L.W, d->bias ? bias : NULL, L.O);
       or_input_checksums(d, L.D, L.cd1, L.cd2);
       or_kernel_checksums(d, L.W, L.cw1, L.cw2);
       double* co[7] = {0, 0, 0, 0, co5, 0, 0};

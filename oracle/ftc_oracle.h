@@ -119,6 +119,16 @@ int or_protected_layer(const or_dims* d, const double* D, const double* W_golden
                        const or_plan* plan, const double* O_conv, const or_pre_fault* pre, int n_pre,
                        or_report* rep, double* O_out);
 
+/* The same with a second seam for BASELINE-scale parity runs: O_recompute, if non-NULL,
+ * stands in for the recompute stage's fresh conv_forward<double> (workflow.hpp:327) --
+ * the GPU's own fault-free FP32 output, widened.  The stage still re-takes the input
+ * checksums, Co5 and So5 and judges them at tau exactly as :325-338; only the O the
+ * check runs on differs (a double conv is consistent to ~1e-15 and always passes, so the
+ * seam can only make the check stricter).  NULL = the reference behaviour. */
+int or_protected_layer_seam(const or_dims* d, const double* D, const double* W_golden, const double* bias,
+                            const or_plan* plan, const double* O_conv, const double* O_recompute,
+                            const or_pre_fault* pre, int n_pre, or_report* rep, double* O_out);
+
 /* One scheme in isolation with the detection + reload preamble and a Co5-only
  * verifier (acceptance.cpp:207-292).  scheme: 1=coc 2=rc 3=clc 4=fc.
  * Returns the CorrectionStatus (or -1 if detection was clean / reload resolved it). */

@@ -211,7 +211,7 @@ def _pre_array(pre):
 
 
 def protected_layer(d: Dims, D, W, bias, rc: bool, clc: bool, tau: float, O_conv=None, pre=None,
-                    want_output=False):
+                    want_output=False, O_recompute=None):
     """run_protected_layer<double> restated; O_conv = the post_conv hook's output.
 
     Inputs D/W/bias are FP32 arrays widened exactly to double."""
@@ -226,8 +226,9 @@ def protected_layer(d: Dims, D, W, bias, rc: bool, clc: bool, tau: float, O_conv
     rep = Report()
     E = extent(d)
     Oout = np.empty((d.N, d.M, E, E)) if want_output else None
-    st = L.or_protected_layer(C.byref(d), P(Dd), P(Wd), P(bd), C.byref(pl), P(Od), pre_arr, npre,
-                              C.byref(rep), P(Oout))
+    Orc = _f64(O_recompute)
+    st = L.or_protected_layer_seam(C.byref(d), P(Dd), P(Wd), P(bd), C.byref(pl), P(Od), P(Orc), pre_arr,
+                                   npre, C.byref(rep), P(Oout))
     res = rep.as_dict()
     res["status"] = st
     res["max_rel_dev"] = rep.max_rel_dev

@@ -16,6 +16,14 @@
 
 #include "ftc_common.cuh"
 
+#ifndef CK
+#define CK(x)                      \
+  do {                             \
+    int _st = (x);                 \
+    if (_st != FTC_OK) return _st; \
+  } while (0)
+#endif
+
 namespace ftc {
 namespace {
 
@@ -196,6 +204,30 @@ int launch_grads(const Bwd& b, const float* D, const float* W, const TG* G, int 
   return FTC_OK;
 }
 
+// Stream-ordered scratch owned by one call: every buffer allocated through it is freed
+// on every return path (early FTC_CUDA_CHECK returns included).
+struct Scratch {
+  cudaStream_t s;
+  void* p[16] = {};
+  int n = 0;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    for (int i = 0; i < n; ++i)
+      if (p[i]) cudaFreeAsync(p[i], s);
+  }
+  template <class T>
+  int alloc(T** out, size_t bytes) {
+    *out = nullptr;
+    if (n == 16) {
+      set_error(FTC_CUDA_ERROR, "backward scratch: too many buffers");
+      return FTC_CUDA_ERROR;
+    }
+    FTC_CUDA_CHECK(cudaMallocAsync((void**)out, bytes, s));
+    p[n++] = (void*)*out;
+    return FTC_OK;
+  }
+};
+
 int round_out(const double* a, float* o, long long n, cudaStream_t s) {
   FTC_LAUNCH(k_round<<<nblocks(n) < 1184 ? nblocks(n) : 1184, kT, 0, s>>>(a, o, n));
   FTC_CUDA_CHECK(cudaGetLastError());
@@ -219,15 +251,13 @@ int ftc_conv_backward(const ftc_conv_desc* desc, const float* D, const float* W,
     return FTC_INVALID_ARGUMENT;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc(s);
   double *w64 = nullptr, *d64 = nullptr;
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&w64, b.nW * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d64, b.nD * sizeof(double), s));
-  st = launch_grads<float>(b, D, W, dO, b.N, b.M, w64, d64, s);
-  if (st == FTC_OK) st = round_out(w64, dW, b.nW, s);
-  if (st == FTC_OK) st = round_out(d64, dD, b.nD, s);
-  cudaFreeAsync(w64, s);
-  cudaFreeAsync(d64, s);
-  return st;
+  CK(sc.alloc(&w64, b.nW * sizeof(double)));
+  CK(sc.alloc(&d64, b.nD * sizeof(double)));
+  CK(launch_grads<float>(b, D, W, dO, b.N, b.M, w64, d64, s));
+  CK(round_out(w64, dW, b.nW, s));
+  return round_out(d64, dD, b.nD, s);
 }
 
 int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const float* W, const float* dO, double tau,
@@ -244,25 +274,21 @@ int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const floa
   cudaStream_t s = (cudaStream_t)stream;
   const long long per_w = (long long)b.C * b.R * b.R, per_d = (long long)b.C * b.H * b.H;
   // scratch: FP64 gradients, block sums, checksum gradients, flags, fault list
+  Scratch sc(s);
   double *w64, *d64, *rows, *cols, *cdw, *cdd;
   int* flags;
   ftc_grad_fault* fl = nullptr;
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&w64, b.nW * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d64, b.nD * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&rows, (size_t)b.N * b.E2 * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&cols, (size_t)b.M * b.E2 * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&cdw, per_w * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&cdd, per_d * sizeof(double), s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&flags, 2 * sizeof(int), s));
+  CK(sc.alloc(&w64, b.nW * sizeof(double)));
+  CK(sc.alloc(&d64, b.nD * sizeof(double)));
+  CK(sc.alloc(&rows, (size_t)b.N * b.E2 * sizeof(double)));
+  CK(sc.alloc(&cols, (size_t)b.M * b.E2 * sizeof(double)));
+  CK(sc.alloc(&cdw, per_w * sizeof(double)));
+  CK(sc.alloc(&cdd, per_d * sizeof(double)));
+  CK(sc.alloc(&flags, 2 * sizeof(int)));
   if (n_hook > 0) {
-    FTC_CUDA_CHECK(cudaMallocAsync((void**)&fl, n_hook * sizeof(ftc_grad_fault), s));
+    CK(sc.alloc(&fl, n_hook * sizeof(ftc_grad_fault)));
     FTC_CUDA_CHECK(cudaMemcpyAsync(fl, hook, n_hook * sizeof(ftc_grad_fault), cudaMemcpyHostToDevice, s));
   }
-  auto cleanup = [&]() {
-    cudaFreeAsync(w64, s); cudaFreeAsync(d64, s); cudaFreeAsync(rows, s); cudaFreeAsync(cols, s);
-    cudaFreeAsync(cdw, s); cudaFreeAsync(cdd, s); cudaFreeAsync(flags, s);
-    if (fl) cudaFreeAsync(fl, s);
-  };
   auto check = [&](int* bad_w, int* bad_d) -> int {
     FTC_CUDA_CHECK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
     FTC_LAUNCH(k_grad_check<<<nblocks(per_w), kT, 0, s>>>(w64, b.M, per_w, cdw, tau, flags));
@@ -300,7 +326,6 @@ int ftc_protected_backward(const ftc_conv_desc* desc, const float* D, const floa
     if ((st = round_out(w64, dW, b.nW, s))) break;
     st = round_out(d64, dD, b.nD, s);
   } while (false);
-  cleanup();
   return st;
 }
 
@@ -318,11 +343,13 @@ static int bwd_host(const ftc_conv_desc* desc, const float* D, const float* W, c
   cudaStream_t s = (cudaStream_t)stream;
   const size_t nW = b.nW * sizeof(float), nD = b.nD * sizeof(float), nO = (size_t)b.N * b.M * b.E2 * sizeof(float);
   float *d_D = nullptr, *d_W = nullptr, *d_O = nullptr, *d_dW = nullptr, *d_dD = nullptr;
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_D, nD, s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_W, nW, s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_O, nO, s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_dW, nW, s));
-  FTC_CUDA_CHECK(cudaMallocAsync((void**)&d_dD, nD, s));
+  {
+  Scratch sc(s);
+  CK(sc.alloc(&d_D, nD));
+  CK(sc.alloc(&d_W, nW));
+  CK(sc.alloc(&d_O, nO));
+  CK(sc.alloc(&d_dW, nW));
+  CK(sc.alloc(&d_dD, nD));
   FTC_CUDA_CHECK(cudaMemcpyAsync(d_D, D, nD, cudaMemcpyHostToDevice, s));
   FTC_CUDA_CHECK(cudaMemcpyAsync(d_W, W, nW, cudaMemcpyHostToDevice, s));
   FTC_CUDA_CHECK(cudaMemcpyAsync(d_O, dO, nO, cudaMemcpyHostToDevice, s));
@@ -332,7 +359,7 @@ static int bwd_host(const ftc_conv_desc* desc, const float* D, const float* W, c
     cudaMemcpyAsync(dW, d_dW, nW, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(dD, d_dD, nD, cudaMemcpyDeviceToHost, s);
   }
-  cudaFreeAsync(d_D, s); cudaFreeAsync(d_W, s); cudaFreeAsync(d_O, s); cudaFreeAsync(d_dW, s); cudaFreeAsync(d_dD, s);
+  }  // scratch freed (stream-ordered) before the synchronisation
   FTC_CUDA_CHECK(cudaStreamSynchronize(s));
   return st;
 }

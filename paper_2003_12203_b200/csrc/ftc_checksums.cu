@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) k_detect_adapt(double* __restrict__ co5,
         const unsigned long long b = (unsigned long long)__double_as_longlong(dev);
         devb = b > devb ? b : devb;
       }
-      bad += values_differ(c, ss, tau) ? 1 : 0;
+      bad += values_differ_guarded(c, ss, tau) ? 1 : 0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(256) k_detect_fused(double* __restrict__ co5, 
     if (den < 1.0) den = 1.0;
     const double dev = fabs(c - ss) / den;
     if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
-    bad = values_differ(c, ss, tau) ? 1 : 0;
+    bad = values_differ_guarded(c, ss, tau) ? 1 : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(256) k_co5_detect(const double* __restrict__ c
     if (den < 1.0) den = 1.0;
     const double dev = fabs(c - ss) / den;
     if (dev == dev && dev > 0.0) devb = (unsigned long long)__double_as_longlong(dev);
-    bad = values_differ(c, ss, tau) ? 1 : 0;
+    bad = values_differ_guarded(c, ss, tau) ? 1 : 0;
   }
   if (t < 32) {  // P <= 32: the compares live in warp 0
 #pragma unroll

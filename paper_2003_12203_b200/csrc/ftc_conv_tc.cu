@@ -1087,15 +1087,34 @@ __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, 
   }
 }
 
-int g_num_sms = 0;
+// Per-device state: the SM count sizes the persistent grid, and the 227 KB dynamic
+// shared-memory opt-in is a per-device function attribute.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
+int num_sms(int dev) {
+  static int sms[kMaxDevices] = {0};
+  if (sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = n > 0 ? n : 148;
+  }
+  return sms[dev];
+}
 
 template <int BN, int MODE, bool FUSE, bool GROUPED>
 int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {false};
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     FTC_CUDA_CHECK(cudaFuncSetAttribute(k_conv_tc<BN, MODE, FUSE, GROUPED>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   FTC_LAUNCH_PDL(k_conv_tc<BN, MODE, FUSE, GROUPED>, dim3(grid), dim3(kThreads), smem, s, a, tm);
   FTC_CUDA_CHECK(cudaGetLastError());
@@ -1324,14 +1343,9 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
   a.rowsum = c.rowsum;
   a.rowsum_m = c.rowsum_m;
   a.plane_mask = c.plane_mask;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+  const int n_sms = num_sms(current_device());
   const int tiles = a.ntiles * a.npt;
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int grid = tiles < n_sms ? tiles : n_sms;
   // as many B stages as shared memory allows (2..8) after the tap table
   const size_t fixed = p->im2col ? 1024 + (size_t)kAS * kAStageBytes + 512 : 1024 + (size_t)p->nkc * kBK * 8 + 512;
   int SB = (int)((227 * 1024 - fixed) / ((size_t)p->BN * 256));

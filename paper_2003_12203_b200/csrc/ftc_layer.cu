@@ -1035,13 +1035,23 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     const bool co5_in = !co5_ready && tc_co5_in_kernel(L->tc, d.N, L->E);
     FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
                    L->fstats_hd, co5_in ? cd1_use : nullptr, L->co5tab};
-    CK(timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready));
-    if (co5_in || co5_ready)
-      CK(launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats,
-                             L->fticket, L->fstats_hd, s));
-    else
-      CK(launch_co5_detect(cd1_use, L->cw1, L->co5f, L->so5acc, d.N, d.C, d.H, d.R, d.stride, d.pad, L->E,
-                           d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats, L->fticket, L->fstats_hd, s));
+    // the staging pass / conv scatter into the Co5 and So5 accumulators, which only
+    // the detect kernels re-zero: on a failed launch clear them here, or every later
+    // call on this layer would read stale partial sums as a CoC-D mismatch
+    int st = timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready);
+    if (st == FTC_OK) {
+      if (co5_in || co5_ready)
+        st = launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau,
+                                 L->fstats, L->fticket, L->fstats_hd, s);
+      else
+        st = launch_co5_detect(cd1_use, L->cw1, L->co5f, L->so5acc, d.N, d.C, d.H, d.R, d.stride, d.pad, L->E,
+                               d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats, L->fticket, L->fstats_hd, s);
+    }
+    if (st != FTC_OK) {
+      cudaMemsetAsync(L->co5f, 0, L->E2 * sizeof(double), s);
+      cudaMemsetAsync(L->so5acc, 0, L->E2 * sizeof(double), s);
+      return st;
+    }
     FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
     L->inflight = true;
     return FTC_OK;

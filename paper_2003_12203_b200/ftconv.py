@@ -162,6 +162,25 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
+def _check_tensor(t, shape, what: str, dtype=None):
+    """Device tensors cross the C ABI as raw pointers: check device, dtype, layout and
+    shape first (a CPU, fp16, strided or undersized tensor would otherwise be read or
+    written out of bounds on the device).  Raises ShapeError like the reference's
+    check_conv_shapes (conv.hpp:16-37)."""
+    torch = _torch()
+    dtype = dtype or torch.float32
+    if not isinstance(t, torch.Tensor):
+        raise ShapeError(f"{what}: expected a torch CUDA tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ShapeError(f"{what}: tensor must live on a CUDA device")
+    if t.dtype != dtype:
+        raise ShapeError(f"{what}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ShapeError(f"{what}: tensor must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ShapeError(f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
 def _stream_ptr(stream) -> int:
     if stream is None:
         return _torch().cuda.current_stream().cuda_stream
@@ -229,6 +248,19 @@ class ProtectedConv:
     def out_shape(self):
         return (self.N, self.M, self.E, self.E)
 
+    @property
+    def in_shape(self):
+        return (self.N, self.C, self.H, self.H)
+
+    def _io(self, D, O):
+        _check_tensor(D, self.in_shape, "D")
+        _check_tensor(O, self.out_shape, "O")
+        if O.device != D.device:
+            raise ShapeError("D and O must live on the same device")
+
+    def _cd(self, cd, what):
+        _check_tensor(cd, (self.C, self.H, self.H), what, _torch().float64)
+
     def _empty_out(self, D):
         torch = _torch()
         return torch.empty(self.out_shape, dtype=torch.float32, device=D.device)
@@ -246,6 +278,7 @@ class ProtectedConv:
     def conv_forward(self, D, O=None, stream=None):
         """conv_forward(D, W, bias, p) on device (conv.hpp:114-131)."""
         O = self._empty_out(D) if O is None else O
+        self._io(D, O)
         _check(_abi.lib().ftc_conv_forward(self.h, _ptr(D), _ptr(O), _stream_ptr(stream)),
                "ftc_conv_forward")
         return O
@@ -253,6 +286,7 @@ class ProtectedConv:
     def protected(self, D, plan: LayerPlan, faults=(), O=None, stream=None):
         """run_protected_layer (workflow.hpp:141-339) on device tensors -> (O, LayerReport)."""
         O = self._empty_out(D) if O is None else O
+        self._io(D, O)
         arr, n = _faults_c(faults)
         rep = _abi.Report()
         pl = plan.c()
@@ -269,6 +303,7 @@ class ProtectedConv:
     def check(self, D, O, plan: LayerPlan, stream=None) -> LayerReport:
         """run_protected_layer on an output O produced elsewhere (post_conv substitution);
         O is repaired in place."""
+        self._io(D, O)
         rep = _abi.Report()
         pl = plan.c()
         _check(_abi.lib().ftc_protected_check(self.h, C.byref(pl), _ptr(D), _ptr(O), C.byref(rep),
@@ -276,6 +311,7 @@ class ProtectedConv:
         return LayerReport.from_c(rep)
 
     def launch(self, D, O, plan: LayerPlan, faults=(), stream=None):
+        self._io(D, O)
         arr, n = _faults_c(faults)
         self._pl = plan.c()
         _check(_abi.lib().ftc_protected_conv_launch(self.h, C.byref(self._pl), _ptr(D), _ptr(O), arr,
@@ -283,6 +319,9 @@ class ProtectedConv:
 
     def launch_ck(self, D, O, cd1, cd2, plan: LayerPlan, faults=(), stream=None):
         """launch with exact input checksums supplied by D's producer (FP64 device tensors)."""
+        self._io(D, O)
+        self._cd(cd1, "cd1")
+        self._cd(cd2, "cd2")
         arr, n = _faults_c(faults)
         self._pl = plan.c()
         _check(_abi.lib().ftc_protected_conv_launch_ck(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
@@ -291,6 +330,10 @@ class ProtectedConv:
     def launch_cd1(self, D, O, cd1, plan: LayerPlan, faults=(), stream=None):
         """launch with the clean-path checksum Cd1 = sum_n D_n (FP64, any order) supplied by
         D's producer, e.g. the start of an ftc_glue_act_pool_cd1 workspace."""
+        self._io(D, O)
+        _check_tensor(cd1, None, "cd1", _torch().float64)
+        if cd1.numel() < self.C * self.H * self.H:
+            raise ShapeError("cd1: workspace smaller than C*H*H")
         arr, n = _faults_c(faults)
         self._pl = plan.c()
         _check(_abi.lib().ftc_protected_conv_launch_cd1(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),

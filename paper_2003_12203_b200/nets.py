@@ -318,11 +318,14 @@ class ProtectedNet:
             reps[op.dst] = rep
             if rep.stage in ("coc", "rc", "clc", "fc", "recompute") and idx < len(ops):
                 # downstream consumed the unrepaired output: finish the stale in-flight
-                # layers, then replay from here with the faults already spent
+                # layers, then replay from here; the downstream layers' own injected
+                # faults are re-applied so each is judged once, on repaired input
                 for op2 in ops[idx:]:
                     if isinstance(op2, Conv):
                         self.layers[op2.dst].finish()
-                self._ops_from(idx, stream, True, None)
+                pending = getattr(self, "_pending_faults", None) or {}
+                rest = {op2.dst for op2 in ops[idx:] if isinstance(op2, Conv)}
+                self._ops_from(idx, stream, True, {k: v for k, v in pending.items() if k in rest})
         return reps
 
     def forward(self, faults=None, stream=None):
@@ -447,44 +450,159 @@ class HostPipeline:
         return reps
 
 
-def calibrate_taus(net, batch, seed, dev, factor=4.0):
-    """tau_L per layer: >= 4x the max fault-free FP64 residual over all
-    seven families of the FP32 output, rounded up to a power of ten."""
+TAU_POLICIES = ("detection", "all-families")
+
+
+def _round_up_125(x: float) -> float:
+    """Smallest value of the 1-2-5 series >= x (plan tau values stay short decimals)."""
+    e = math.floor(math.log10(x))
+    for m in (1.0, 2.0, 5.0, 10.0):
+        v = float(f"{m}e{e}")
+        if v >= x * (1 - 1e-12):
+            return v
+    return float(f"1e{e + 1}")
+
+
+def layer_residuals(net, batch, weight_seed, dev, inputs):
+    """Fault-free FP64 residuals of every protected layer on the given inputs.
+
+    For each conv and each input batch: the max relative residual
+    |C-S|/max(|C|,|S|,1) of all seven checksum families (Co1..Co7 against So1..So7, the
+    values_differ metric of checksums.hpp:54-60) and the median of max(|Co5|,|So5|,1)
+    over positions (the CoC-D denominator).  Returns {layer: {"res": [7 floats],
+    "den5_median": float}} (max over the inputs)."""
     import torch
     from .ftconv import input_checksums, output_checksums, output_summations
-    pn = ProtectedNet(net, batch, seed, dev)
-    pn.set_input(torch.from_numpy(net_input(net, batch, seed)).to(dev))
-    pn.unprotected()
+    pn = ProtectedNet(net, batch, weight_seed, dev)
+    out = {}
+    try:
+        for x in inputs:
+            pn.set_input(torch.from_numpy(np.ascontiguousarray(x)).to(dev))
+            pn.unprotected()
+            for op, Cin, H, E in pn.convs:
+                L = pn.layers[op.dst]
+                W = torch.from_numpy(pn.weights[op.dst][0]).to(dev)
+                b = pn.weights[op.dst][1]
+                D = pn.buf[op.src]
+                ic = input_checksums(D, W, 1)
+                cs = output_checksums(127, D, W, ic, L.p)
+                so = output_summations(pn.buf[op.dst], 127, torch.from_numpy(b).to(dev) if b is not None else None)
+                res = []
+                for c, sm in zip(cs, so):
+                    den = torch.clamp(torch.maximum(c.abs(), sm.abs()), min=1.0)
+                    res.append(float(((c - sm).abs() / den).max()))
+                den5 = torch.clamp(torch.maximum(cs[4].abs(), so[4].abs()), min=1.0)
+                rec = out.setdefault(op.dst, {"res": [0.0] * 7, "den5_median": 0.0})
+                rec["res"] = [max(a, b_) for a, b_ in zip(rec["res"], res)]
+                rec["den5_median"] = max(rec["den5_median"], float(den5.median()))
+        torch.cuda.synchronize()
+    finally:
+        pn.close()
+    return out
+
+
+def taus_from_residuals(res, policy="detection", factor=4.0):
+    """tau_L per layer from layer_residuals():
+
+    * "all-families": >= factor x the max residual over all seven
+      families, rounded up to a power of ten -- no family false-flags, so CoC/RC/ClC
+      corrections verify; the CoC-D floor is coarse (the m/n-weighted families carry
+      the largest FP32-output noise).
+    * "detection": factor x the Co5/So5 residual alone, rounded up in the 1-2-5 series --
+      the finest floor at which fault-free CoC-D stays clean; the weighted families may
+      then fail the verifier, so correction falls over to the reference's own recompute
+      stage (workflow.hpp:325-338).
+    The same tau goes to the device and the oracle, so verdict parity is policy-free."""
     taus = {}
-    for op, Cin, H, E in pn.convs:
-        L = pn.layers[op.dst]
-        W = torch.from_numpy(pn.weights[op.dst][0]).to(dev)
-        b = pn.weights[op.dst][1]
-        D = pn.buf[op.src]
-        ic = input_checksums(D, W, 1)
-        cs = output_checksums(127, D, W, ic, L.p)
-        so = output_summations(pn.buf[op.dst], 127, torch.from_numpy(b).to(dev) if b is not None else None)
-        worst = 0.0
-        for c, s in zip(cs, so):
-            den = torch.clamp(torch.maximum(c.abs(), s.abs()), min=1.0)
-            worst = max(worst, float(((c - s).abs() / den).max()))
-        taus[op.dst] = 10.0 ** math.ceil(math.log10(max(worst * factor, 1e-7)))
-    torch.cuda.synchronize()
-    pn.close()
+    for k, r in res.items():
+        if policy == "all-families":
+            taus[k] = 10.0 ** math.ceil(math.log10(max(max(r["res"]) * factor, 1e-7)))
+        elif policy == "detection":
+            taus[k] = _round_up_125(max(r["res"][4] * factor, 1e-7))
+        else:
+            raise ValueError(f"unknown tau policy {policy!r}")
     return taus
 
 
-class BenchNet:
-    """bench.py adapter: protected forward of one shard, unprotected forward, e2e."""
+def detection_floor(res, taus):
+    """Per layer: the smallest |delta| CoC-D flags at a typical position,
+    tau_L * median max(|Co5|,|So5|,1) (replay.hpp:78-95 classifies detectability at
+    10*tau on the same scale)."""
+    return {k: taus[k] * res[k]["den5_median"] for k in taus}
 
-    def __init__(self, name, seed, dev):
+
+def calibrate_taus(net, batch, seed, dev, factor=4.0, policy="all-families", inputs=None):
+    """tau_L per layer on `inputs` (default: the net's seeded input `seed`)."""
+    if inputs is None:
+        inputs = [net_input(net, batch, seed)]
+    return taus_from_residuals(layer_residuals(net, batch, 11, dev, inputs), policy, factor)
+
+
+def fault_plan(name, convs, batch, run, base=9000):
+    """Seeded output bit flips (bits 20-30, as configs[0]) for faulted forward `run` of
+    net `name`, following the BASELINE configs' injection rules:
+
+    * alexnet: one flip in every conv ("one seeded output bit-flip per layer");
+    * vgg19, resnet18: one flip in each of ceil(10% of the convs) seeded layers;
+    * yolov2: two seeded layers with 1-3 flips each, cycling through the patterns the
+      RC/ClC localisation targets -- same image (one row of the (n, m) block grid),
+      same kernel (one column), scattered.
+
+    Returns {layer: [(n, m, x, y, bit), ...]} in shard-local coordinates."""
+    L = len(convs)
+    g = np.random.default_rng(synth.splitmix64((base * 7919) ^ run))
+    if name == "alexnet":
+        chosen = list(range(L))
+    elif name == "yolov2":
+        chosen = sorted(g.choice(L, size=min(2, L), replace=False).tolist())
+    else:
+        chosen = sorted(g.choice(L, size=max(1, math.ceil(0.1 * L)), replace=False).tolist())
+    plan = {}
+    for li in chosen:
+        op, Cin, H, E = convs[li]
+        if name != "yolov2":
+            n, m, x, y, bit = synth.flip_sample(base + li, run, batch, op.M, E)
+            plan[op.dst] = [(n, m, x, y, bit)]
+            continue
+        k = int(g.integers(1, 4))
+        pattern = run % 3
+        n0, m0 = int(g.integers(0, batch)), int(g.integers(0, op.M))
+        ns = [n0] * k if pattern == 0 else list(g.choice(batch, size=min(k, batch), replace=False))
+        ms = [m0] * k if pattern == 1 else list(g.choice(op.M, size=k, replace=False))
+        flips = []
+        for n, m in zip(ns, ms):
+            flips.append((int(n), int(m), int(g.integers(0, E)), int(g.integers(0, E)), int(g.integers(20, 31))))
+        plan[op.dst] = flips
+    return plan
+
+
+REPAIRED = ("coc", "rc", "clc", "fc", "recompute")
+
+
+class BenchNet:
+    """bench.py adapter: protected forward of one batch shard, unprotected forward, e2e,
+    faulted forwards under either tau policy.
+
+    The shard is images [lo, hi) of the config's global batch (dist.shard_range); its
+    inputs are the matching slice of the seeded global input, and its tau_L are
+    calibrated on its own shard (shard-local N: SURVEY 8(e))."""
+
+    def __init__(self, name, dev, policy="detection", shard=None, input_seed=1000, calib_seeds=(11, 12)):
         import torch
         net = NETS[name]()
-        self.net = net
-        self.batch = net["batch"]
-        self.taus = calibrate_taus(net, self.batch, 11, dev)
+        self.name, self.net, self.dev = name, net, dev
+        self.global_batch = net["batch"]
+        lo, hi = shard if shard is not None else (0, self.global_batch)
+        self.lo, self.hi = lo, hi
+        self.batch = hi - lo
+        calib = [net_input(net, self.global_batch, s)[lo:hi] for s in calib_seeds]
+        self.residuals = layer_residuals(net, self.batch, 11, dev, calib)
+        self.taus_by_policy = {p: taus_from_residuals(self.residuals, p) for p in TAU_POLICIES}
+        self.floors_by_policy = {p: detection_floor(self.residuals, t) for p, t in self.taus_by_policy.items()}
+        self.policy = policy
+        self.taus = self.taus_by_policy[policy]
         self.pn = ProtectedNet(net, self.batch, 11, dev, self.taus)
-        x = net_input(net, self.batch, seed)
+        x = np.ascontiguousarray(net_input(net, self.global_batch, input_seed)[lo:hi])
         self.x_host = torch.from_numpy(x).pin_memory()
         self.pn.set_input(self.x_host.to(dev))
         self.layers = list(self.pn.layers.values())
@@ -493,6 +611,12 @@ class BenchNet:
         self.out_host = torch.empty(out.shape, dtype=torch.float32).pin_memory()
         self.in_bytes = x.nbytes
         self.out_bytes = self.out_host.numel() * 4
+
+    def set_policy(self, policy):
+        self.policy = policy
+        self.taus = self.taus_by_policy[policy]
+        for k, pl in self.pn.plans.items():
+            pl.tau = self.taus[k]
 
     def launch(self):
         self.pn.launch()
@@ -511,21 +635,58 @@ class BenchNet:
         self.pn.torch.cuda.current_stream().synchronize()
         return list(reps.values())
 
-    def faulted(self, run: int):
-        """One protected forward with one seeded output bit flip (bits 20-30) in every conv
-        (BASELINE configs: "one seeded output bit-flip per layer") -> (verdicts, output
-        equals the fault-free one)."""
+    def faults_for(self, run):
         from .ftconv import output_bitflip
+        plan = fault_plan(self.name, self.pn.convs, self.batch, run)
+        return plan, {k: [output_bitflip(*f) for f in v] for k, v in plan.items()}
+
+    def faulted(self, run: int):
+        """One protected forward with fault_plan(run) -> (plan, {layer: LayerReport},
+        output equals the fault-free output)."""
         if not hasattr(self, "clean_out"):
             self.pn.forward()
             self.clean_out = self.pn.output().clone()
-        faults = {}
-        for li, (op, Cin, H, E) in enumerate(self.pn.convs):
-            n, m, x, y, bit = synth.flip_sample(9000 + li, run, self.batch, op.M, E)
-            faults[op.dst] = [output_bitflip(n, m, x, y, bit)]
+        plan, faults = self.faults_for(run)
         reps = self.pn.forward(faults)
         same = bool(self.pn.torch.equal(self.pn.output(), self.clean_out))
-        return list(reps.values()), same
+        return plan, reps, same
+
+    def campaign(self, runs: int):
+        """`runs` faulted forwards under the current policy -> coverage summary."""
+        import time
+        torch = self.pn.torch
+        inj = det = fp = 0
+        by_bit, stages = {}, {}
+        repaired_runs, equal_runs = 0, 0
+        t = 0.0
+        for r in range(runs):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            plan, reps, same = self.faulted(r)
+            torch.cuda.synchronize()
+            t += time.perf_counter() - t0
+            for name, rep in reps.items():
+                if name not in plan:
+                    fp += int(rep.detected)
+                    continue
+                stages[rep.stage] = stages.get(rep.stage, 0) + 1
+                det += int(rep.detected)
+                for (_, _, _, _, bit) in plan[name]:
+                    inj += 1
+                    b = by_bit.setdefault(str(bit), [0, 0])
+                    b[0] += int(rep.detected)
+                    b[1] += 1
+            if all(reps[k].stage in REPAIRED for k in plan):
+                repaired_runs += 1
+                equal_runs += int(same)
+        return {"policy": self.policy, "runs": runs, "faulted_layers": sum(stages.values()),
+                "flips_injected": inj, "faulted_layers_detected": det, "false_positive_layers": fp,
+                "detected_by_bit": dict(sorted(by_bit.items(), key=lambda kv: int(kv[0]))),
+                "stages": stages, "fully_repaired_runs": repaired_runs,
+                "fully_repaired_output_equals_fault_free": (equal_runs == repaired_runs) if repaired_runs else None,
+                "ms_per_faulted_forward": 1e3 * t / max(1, runs),
+                "tau_per_layer": dict(self.taus),
+                "detection_floor_per_layer": {k: float(f"{v:.3g}") for k, v in self.floors_by_policy[self.policy].items()}}
 
     def e2e_stream(self, steps, before_step=None, start_event=None):
         """`steps` host batches through HostPipeline (H2D/D2H overlapped with compute)."""
@@ -539,55 +700,7 @@ class BenchNet:
                              before_step, start_event)
         return [list(r.values()) for r in reps]
 
-
-# ----------------------------------------------------------------------------- CPU reference
-def _np_act_pool(x, act, k, s, p):
-    if act == "relu":
-        x = np.maximum(x, 0)
-    elif act == "leaky":
-        x = np.where(x > 0, x, np.float32(0.1) * x)
-    if k == 1 and s == 1 and p == 0:
-        return x.astype(np.float32)
-    N, Cc, H, _ = x.shape
-    Ho = (H + 2 * p - k) // s + 1
-    xp = np.full((N, Cc, H + 2 * p, H + 2 * p), -np.inf, np.float32)
-    xp[:, :, p:p + H, p:p + H] = x
-    out = np.full((N, Cc, Ho, Ho), -np.inf, np.float32)
-    for i in range(k):
-        for j in range(k):
-            out = np.maximum(out, xp[:, :, i:i + s * Ho:s, j:j + s * Ho:s][:, :, :Ho, :Ho])
-    return out
-
-
-def reference_forward(name, seed, images):
-    """The reference's shipped CPU path through the whole net on `images` images:
-    run_protected_layer<float> (make_default_plan, tau 1e-4, ConvImpl::direct) per
-    conv via oracle/_ref, numpy glue in between.  Used for bench.py's CPU baseline."""
-    import os
-    import sys
-    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    sys.path.insert(0, os.path.join(here, "oracle"))
-    import oracle_py as O
-    net = NETS[name]()
-    sh, convs = shapes(net)
-    wts = net_weights(net, 11)
-    t = {"x": net_input(net, images, seed)}
-    for op in net["ops"]:
-        if isinstance(op, Conv):
-            W, b = wts[op.dst]
-            Cin, H = sh[op.src]
-            d = O.dims(images, Cin, H, op.M, op.R, op.stride, op.pad, 1, op.bias)
-            _, t[op.dst] = O.ref_protected_layer_f32(d, t[op.src], W, b, tau=1e-4)
-        elif isinstance(op, ActPool):
-            t[op.dst] = _np_act_pool(t[op.src], op.act, op.k, op.s, op.p)
-        elif isinstance(op, AddAct):
-            t[op.dst] = _np_act_pool(t[op.a] + t[op.b], op.act, 1, 1, 0)
-        elif isinstance(op, PadCrop):
-            x = t[op.src]
-            H = x.shape[2]
-            Ho = H + op.lo + op.hi
-            y = np.zeros(x.shape[:2] + (Ho, Ho), np.float32)
-            src = x[:, :, :min(H, Ho - op.lo), :min(H, Ho - op.lo)]
-            y[:, :, op.lo:op.lo + src.shape[2], op.lo:op.lo + src.shape[3]] = src
-            t[op.dst] = y
-    return t
+    def close(self):
+        self.pn.close()
+        if hasattr(self, "pn2"):
+            self.pn2.close()

@@ -38,11 +38,29 @@ def _rep(rank, layer):
 
 def test_pack_roundtrip():
     reps = [_rep(1, l) for l in range(5)]
-    back = D.unpack_reports(D.pack_reports(reps))
+    back = D.unpack_reports(D.pack_reports(reps, lo=32))
     for r, b in zip(reps, back):
         assert b["detected"] == r.detected and b["stage"] == r.stage
         assert b["stages_attempted"] == r.stages_attempted
         assert b["max_rel_dev"] == r.max_rel_dev
+        assert b["corrected_blocks"] == list(r.corrected_blocks)
+        assert b["image_offset"] == 32 and not b["blocks_truncated"]
+
+
+def test_pack_keeps_every_block_up_to_capacity():
+    """A row correction lists one block per kernel: the record carries the full list up
+    to BLOCK_CAP plus the true count (and flags truncation beyond it)."""
+    many = [(3, j) for j in range(D.BLOCK_CAP + 10)]
+    r = LayerReport(detected=True, stage="rc", corrected_blocks=many, stages_attempted=["coc", "rc"],
+                    n_blocks=len(many))
+    few = LayerReport(detected=True, stage="rc", corrected_blocks=many[:40], stages_attempted=["coc", "rc"],
+                      n_blocks=40)
+    b_many, b_few = D.unpack_reports(D.pack_reports([r, few], lo=8))
+    assert b_few["corrected_blocks"] == many[:40] and not b_few["blocks_truncated"]
+    assert b_many["n_blocks"] == len(many) and b_many["blocks_truncated"]
+    assert b_many["corrected_blocks"] == many[:D.BLOCK_CAP]
+    glob = D.global_blocks([[D.unpack_reports(D.pack_reports([few], lo=8))[0]]])
+    assert glob[0] == [(11, j) for j in range(40)]
 
 
 def _worker(rank, world, port, q):
@@ -55,6 +73,40 @@ def _worker(rank, world, port, q):
     q.put((rank, [[rec["stage"] for rec in shard] for shard in table], D.summarize(table)))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _shard_worker(rank, world, port, q):
+    """The bench's sharded harness minus the device: shard the global batch, report
+    shard-local blocks, all-gather the packed records, map them to global images."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = D.shard_range(64, world, rank)
+    reps = [LayerReport(detected=True, stage="coc", corrected_blocks=[(hi - lo - 1, 5 + rank)],
+                        stages_attempted=["coc"], n_blocks=1),
+            LayerReport()]
+    table = D.gather_verdicts(reps, lo=lo)
+    q.put((rank, D.global_blocks(table), D.summarize(table)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_verdicts_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, glob, summ in got:
+        # shard 0 owns images 0..31, shard 1 32..63; each corrected its last local image
+        assert glob == {0: [(31, 5), (63, 6)]}
+        assert summ["shards"] == 2 and summ["detected"] == 2 and summ["corrected_blocks"] == 2
 
 
 def _free_port():

@@ -6,7 +6,7 @@ import torch
 from paper_2003_12203_b200 import nets, _abi
 from paper_2003_12203_b200.ftconv import output_bitflip
 from paper_2003_12203_b200 import synth
-bn = nets.BenchNet("alexnet", 1000, torch.device("cuda"))
+bn = nets.BenchNet("alexnet", torch.device("cuda"), policy="all-families")
 bn.pn.forward(); torch.cuda.synchronize()
 lib = _abi.lib()
 for run in range(3):
