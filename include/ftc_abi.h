@@ -190,6 +190,21 @@ int ftc_protected_conv_host(ftc_layer* layer, const ftc_plan* plan, const float*
 int ftc_protected_conv_launch(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
                               const ftc_fault* faults, int32_t n_faults, void* stream);
 int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
+/* Abandon the call in flight (a pipeline replays it on repaired input): waits for the
+ * clean path to drain and drops its verdict without running the error path. */
+int ftc_protected_conv_cancel(ftc_layer* layer);
+
+/* One correcting scheme in isolation -- the reference's acceptance criterion C4
+ * (proj/tests/acceptance.cpp:207-292, isolation_succeeds): the clean path and the
+ * detection + verify_kernel/reload preamble of run_protected_layer, then ONLY `scheme`
+ * (FTC_SCHEME_COC/RC/CLC/FC) with a Co5-only verifier (:247-251) and no CoC probes.
+ * *status: -1 settled by the preamble (clean, or clean after a reload), 0 corrected
+ * (the corrected (n,m) planes are recomputed in O; report->corrected_blocks lists them),
+ * 1 discard (checksum corruption), 2 escalate (O holds the unrepaired output). */
+enum { FTC_SCHEME_COC = 1, FTC_SCHEME_RC = 2, FTC_SCHEME_CLC = 3, FTC_SCHEME_FC = 4 };
+int ftc_isolated_scheme(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
+                        const ftc_fault* faults, int32_t n_faults, int32_t scheme, int32_t* status,
+                        ftc_layer_report* report, void* stream);
 
 /* _launch with the input checksums supplied by the producer of D: cd1/cd2 are
  * device FP64 C*H*H tensors holding sum_n D_n and sum_n n*D_n in ascending n

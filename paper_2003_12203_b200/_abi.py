@@ -29,7 +29,8 @@ EXPORTS = (
     "ftc_cost_model", "ftc_decide_rc", "ftc_decide_clc", "ftc_estimate_error_probs", "ftc_make_default_plan",
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
     "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
-    "ftc_conv_backward_host", "ftc_protected_backward_host",
+    "ftc_conv_backward_host", "ftc_protected_backward_host", "ftc_isolated_scheme",
+    "ftc_protected_conv_cancel",
 )
 
 
@@ -121,6 +122,9 @@ def lib():
         L.ftc_protected_conv_launch.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32,
                                                 vp]
         L.ftc_protected_conv_finish.argtypes = [vp, C.POINTER(Report)]
+        L.ftc_protected_conv_cancel.argtypes = [vp]
+        L.ftc_isolated_scheme.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32, i32,
+                                          C.POINTER(i32), C.POINTER(Report), vp]
         L.ftc_input_checksums.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp]
         L.ftc_kernel_checksums.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp]
         L.ftc_output_checksums.argtypes = [C.POINTER(ConvDesc), u32, vp, vp, vp, vp, vp, vp,

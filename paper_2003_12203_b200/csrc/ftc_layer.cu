@@ -325,6 +325,9 @@ struct EP {
   cudaStream_t s;
   unsigned cs_have = 0, s_have = 0;
   bool ov_dirty = false;
+  // families the verifier may trust (further restricted to what was computed): the
+  // workflow's {O1,O3,O5,O6,O7}; {O5} for one scheme in isolation (acceptance.cpp:247-251)
+  unsigned trust_mask = FTC_CK_O1 | FTC_CK_O3 | FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7;
 };
 
 VirtualO vobj(EP& e) {
@@ -450,7 +453,7 @@ int probe(EP& e, bool row0, bool* consistent) {
 // workflow.hpp:205-219 over the current patch list; on failure roll back.
 int verify_patches(EP& e, int np, bool* pass) {
   ftc_layer* L = e.L;
-  const unsigned trusted = e.cs_have & (FTC_CK_O1 | FTC_CK_O3 | FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7);
+  const unsigned trusted = e.cs_have & e.trust_mask;
   VerifyWS ws{L->ov, L->present, L->touched5, L->touched1};
   CK(run_verify(fam(e), trusted, L->O, L->d.N, L->d.M, L->E2, L->d.bias_enabled, L->bias, L->agg,
                 L->plan.tau, L->patches, L->res, np, ws, L->iscratch, e.s));
@@ -513,19 +516,23 @@ int finish_valid(EP& e, int stage, ftc_layer_report* rep, int* settled) {
   return FTC_OK;
 }
 
-int error_path(ftc_layer* L, ftc_layer_report* rep) {
-  CK(alloc_error_path(L));
-  EP e{L, L->stream};
+int clear_overrides(EP& e) {
+  ftc_layer* L = e.L;
+  if (e.ov_dirty) {
+    FTC_CUDA_CHECK(cudaMemsetAsync(L->present, 0, L->nO, e.s));
+    FTC_CUDA_CHECK(cudaMemsetAsync(L->touched5, 0, L->E2, e.s));
+    FTC_CUDA_CHECK(cudaMemsetAsync(L->touched1, 0, (size_t)L->d.M * L->E2, e.s));
+  }
+  return FTC_OK;
+}
+
+// workflow.hpp:221-245: exact-order input checksums, CoC-D on exact-order Co5/So5, and
+// verify_kernel / reload.  *resolved = 1 when the layer is settled here (clean on the
+// exact re-detection, or clean after the reload).
+int detect_and_reload(EP& e, ftc_layer_report* rep, int* resolved) {
+  ftc_layer* L = e.L;
   const ftc_conv_desc& d = L->d;
-  int ret = FTC_OK;
-  auto cleanup = [&]() -> int {
-    if (e.ov_dirty) {
-      FTC_CUDA_CHECK(cudaMemsetAsync(L->present, 0, L->nO, e.s));
-      FTC_CUDA_CHECK(cudaMemsetAsync(L->touched5, 0, L->E2, e.s));
-      FTC_CUDA_CHECK(cudaMemsetAsync(L->touched1, 0, (size_t)d.M * L->E2, e.s));
-    }
-    return FTC_OK;
-  };
+  *resolved = 0;
 
   // The clean path may have produced only a fast Cd1: take the exact-order input
   // checksums of the caller's (pre-fault) D, re-applying injected checksum faults.
@@ -553,7 +560,8 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
   rep->detected = !clean;
   if (clean) {
     rep->stage = FTC_STAGE_NONE;
-    return cleanup();
+    *resolved = 1;
+    return FTC_OK;
   }
 
   // verify_kernel (checksums.hpp:250-259) / reload (workflow.hpp:232-245)
@@ -570,9 +578,22 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
     CK(detect_exact_clean(e, &clean, nullptr));
     if (clean) {
       rep->stage = FTC_STAGE_RELOAD;
-      return cleanup();
+      *resolved = 1;
     }
   }
+  return FTC_OK;
+}
+
+int error_path(ftc_layer* L, ftc_layer_report* rep) {
+  CK(alloc_error_path(L));
+  EP e{L, L->stream};
+  const ftc_conv_desc& d = L->d;
+  int ret = FTC_OK;
+  auto cleanup = [&]() -> int { return clear_overrides(e); };
+  bool clean = false;
+  int resolved = 0;
+  CK(detect_and_reload(e, rep, &resolved));
+  if (resolved) return cleanup();
 
   // CoC (workflow.hpp:277-288)
   CK(ensure_cs(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
@@ -664,6 +685,70 @@ int error_path(ftc_layer* L, ftc_layer_report* rep) {
   ret = FTC_INTEGRITY_ERROR;
   set_error(ret, "layer recomputation failed verification twice");
   return ret;
+}
+
+// acceptance.cpp:207-292 (isolation_succeeds): the detection + reload preamble, then ONE
+// scheme on its own with a Co5-only verifier and no CoC probes (an index-0 pattern is a
+// discard).  *status: -1 settled by the preamble (clean / reload), 0 corrected (planes
+// repaired), 1 discard, 2 escalate (patches rolled back, O untouched).
+int isolated_path(ftc_layer* L, int scheme, int* status, ftc_layer_report* rep) {
+  CK(alloc_error_path(L));
+  EP e{L, L->stream};
+  e.trust_mask = FTC_CK_O5;
+  const ftc_conv_desc& d = L->d;
+  auto cleanup = [&]() -> int { return clear_overrides(e); };
+  int resolved = 0;
+  *status = -1;
+  CK(detect_and_reload(e, rep, &resolved));
+  if (resolved) return cleanup();
+  int settled = 0;
+  *status = 2;
+  if (scheme == 1) {
+    CK(ensure_cs(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+    CK(ensure_s(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+    add_stage(rep, FTC_STAGE_COC);
+    CK(run_coc_analyze(fam(e), d.N, d.M, L->E2, L->plan.tau, L->res, L->patches, e.s));
+    CK(sync_result(e));
+    switch (L->res_h->status) {
+      case SCH_EMPTY: *status = 0; break;
+      case SCH_VALID:
+        CK(finish_valid(e, FTC_STAGE_COC, rep, &settled));
+        *status = settled ? 0 : 2;
+        break;
+      case SCH_PROBE_ROW0:
+      case SCH_PROBE_COL0: *status = 1; break;
+      default: break;
+    }
+  } else if (scheme == 2 || scheme == 3) {
+    const bool rc = scheme == 2;
+    const unsigned fams = rc ? (FTC_CK_O1 | FTC_CK_O3) : (FTC_CK_O2 | FTC_CK_O4);
+    CK(ensure_cs(e, fams));
+    CK(ensure_s(e, fams));
+    add_stage(rep, rc ? FTC_STAGE_RC : FTC_STAGE_CLC);
+    CK(run_line_analyze(fam(e), rc, d.N, d.M, L->E2, L->plan.tau, L->res, L->patches, e.s));
+    CK(sync_result(e));
+    if (L->res_h->status == SCH_EMPTY) {
+      *status = 0;
+    } else if (L->res_h->status == SCH_VALID) {
+      CK(finish_valid(e, rc ? FTC_STAGE_RC : FTC_STAGE_CLC, rep, &settled));
+      *status = settled ? 0 : 2;
+    }
+  } else {
+    CK(ensure_cs(e, FTC_CK_O1 | FTC_CK_O2 | FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+    CK(ensure_s(e, FTC_CK_O1 | FTC_CK_O2 | FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+    add_stage(rep, FTC_STAGE_FC);
+    CK(run_fc_analyze(fam(e), d.N, d.M, L->E2, L->plan.tau, L->res, L->patches, L->colmask,
+                      L->rowmask, L->colany, L->rowany, e.s));
+    CK(sync_result(e));
+    if (L->res_h->status == SCH_DISCARD) {
+      *status = 1;
+    } else if (L->res_h->status == SCH_VALID) {
+      CK(finish_valid(e, FTC_STAGE_FC, rep, &settled));
+      *status = settled ? 0 : 2;
+    }
+  }
+  if (*status == 1) rep->stage = FTC_STAGE_DISCARD;
+  return cleanup();
 }
 
 int stage_faults(ftc_layer* L, const ftc_fault* faults, int n, cudaStream_t s) {
@@ -1179,6 +1264,35 @@ int ftc_protected_conv(ftc_layer* L, const ftc_plan* plan, const float* D, float
                        void* stream) {
   CK(ftc_protected_conv_launch(L, plan, D, O, faults, n_faults, stream));
   return ftc_protected_conv_finish(L, rep);
+}
+
+int ftc_protected_conv_cancel(ftc_layer* L) {
+  if (!L) RET_ERR(FTC_INVALID_ARGUMENT, "null layer");
+  if (!L->inflight) return FTC_OK;
+  L->inflight = false;
+  // the clean path re-arms its accumulators itself; only wait for it to drain
+  FTC_CUDA_CHECK(cudaEventSynchronize(L->ev_done));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int ftc_isolated_scheme(ftc_layer* L, const ftc_plan* plan, const float* D, float* O, const ftc_fault* faults,
+                        int32_t n_faults, int32_t scheme, int32_t* status, ftc_layer_report* rep, void* stream) {
+  if (!L || !rep || !status) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (scheme < FTC_SCHEME_COC || scheme > FTC_SCHEME_FC) RET_ERR(FTC_CONFIG_ERROR, "scheme must be 1..4");
+  CK(ftc_protected_conv_launch(L, plan, D, O, faults, n_faults, stream));
+  L->inflight = false;
+  std::memset(rep, 0, sizeof *rep);
+  FTC_CUDA_CHECK(cudaEventSynchronize(L->ev_done));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  const int flagged = ((volatile DetectStats*)L->fstats_h)->flagged;
+  rep->n_flagged = flagged;
+  *status = -1;
+  if (flagged == 0) {
+    rep->stage = FTC_STAGE_NONE;
+    return FTC_OK;
+  }
+  return isolated_path(L, scheme, status, rep);
 }
 
 int ftc_protected_conv_host(ftc_layer* L, const ftc_plan* plan, const float* D_host, float* O_host,

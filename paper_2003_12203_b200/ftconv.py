@@ -95,6 +95,7 @@ class LayerReport:
     n_blocks: int = 0
     repaired_planes: int = 0
     timings: dict = field(default_factory=dict)
+    integrity_error: bool = False  # recompute failed twice (the reference throws IntegrityError)
 
     @staticmethod
     def from_c(r: _abi.Report) -> "LayerReport":
@@ -310,6 +311,23 @@ class ProtectedConv:
                                               _stream_ptr(stream)), "ftc_protected_check")
         return LayerReport.from_c(rep)
 
+    def isolated(self, D, plan: LayerPlan, scheme: str, faults=(), O=None, stream=None):
+        """One scheme in isolation (acceptance.cpp:207-292): detection + reload preamble,
+        then only `scheme` ("coc" | "rc" | "clc" | "fc") with a Co5-only verifier.
+        Returns (O, status, LayerReport); status is "clean" (settled by the preamble),
+        "corrected", "discard" or "escalate"."""
+        O = self._empty_out(D) if O is None else O
+        self._io(D, O)
+        arr, n = _faults_c(faults)
+        rep = _abi.Report()
+        pl = plan.c()
+        st = C.c_int32()
+        code = {"coc": 1, "rc": 2, "clc": 3, "fc": 4}[scheme]
+        _check(_abi.lib().ftc_isolated_scheme(self.h, C.byref(pl), _ptr(D), _ptr(O), arr, n, code, C.byref(st),
+                                              C.byref(rep), _stream_ptr(stream)), "ftc_isolated_scheme")
+        names = {-1: "clean", 0: "corrected", 1: "discard", 2: "escalate"}
+        return O, names[st.value], LayerReport.from_c(rep)
+
     def launch(self, D, O, plan: LayerPlan, faults=(), stream=None):
         self._io(D, O)
         arr, n = _faults_c(faults)
@@ -339,9 +357,18 @@ class ProtectedConv:
         _check(_abi.lib().ftc_protected_conv_launch_cd1(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
                                                         arr, n, _stream_ptr(stream)), "launch_cd1")
 
+    def cancel(self) -> None:
+        """Drop the call in flight without judging it (its input was stale)."""
+        _check(_abi.lib().ftc_protected_conv_cancel(self.h), "cancel")
+
     def finish(self) -> LayerReport:
         rep = _abi.Report()
-        _check(_abi.lib().ftc_protected_conv_finish(self.h, C.byref(rep)), "finish")
+        st = _abi.lib().ftc_protected_conv_finish(self.h, C.byref(rep))
+        if st == 4:  # FTC_INTEGRITY_ERROR: the report is filled (workflow.hpp:325-338)
+            err = IntegrityError(f"finish: {_abi.last_error()}")
+            err.report = LayerReport.from_c(rep)
+            raise err
+        _check(st, "finish")
         return LayerReport.from_c(rep)
 
     def protected_host(self, D: np.ndarray, plan: LayerPlan, faults=(), O: np.ndarray | None = None,

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi, synth
-from .ftconv import ConvParams, LayerPlan, ProtectedConv, _check
+from .ftconv import ConvParams, IntegrityError, LayerPlan, ProtectedConv, _check
 
 ACT = {"none": 0, "relu": 1, "leaky": 2}
 
@@ -313,7 +313,13 @@ class ProtectedNet:
             idx += 1
             if not isinstance(op, Conv):
                 continue
-            rep = self.layers[op.dst].finish()
+            try:
+                rep = self.layers[op.dst].finish()
+            except IntegrityError as err:
+                # recomputation failed verification twice (workflow.hpp:338): the
+                # reference throws; a pipeline records it and carries on
+                rep = err.report
+                rep.integrity_error = True
             rep.layer = op.dst
             reps[op.dst] = rep
             if rep.stage in ("coc", "rc", "clc", "fc", "recompute") and idx < len(ops):
@@ -322,7 +328,7 @@ class ProtectedNet:
                 # faults are re-applied so each is judged once, on repaired input
                 for op2 in ops[idx:]:
                     if isinstance(op2, Conv):
-                        self.layers[op2.dst].finish()
+                        self.layers[op2.dst].cancel()
                 pending = getattr(self, "_pending_faults", None) or {}
                 rest = {op2.dst for op2 in ops[idx:] if isinstance(op2, Conv)}
                 self._ops_from(idx, stream, True, {k: v for k, v in pending.items() if k in rest})
@@ -468,9 +474,10 @@ def layer_residuals(net, batch, weight_seed, dev, inputs):
 
     For each conv and each input batch: the max relative residual
     |C-S|/max(|C|,|S|,1) of all seven checksum families (Co1..Co7 against So1..So7, the
-    values_differ metric of checksums.hpp:54-60) and the median of max(|Co5|,|So5|,1)
-    over positions (the CoC-D denominator).  Returns {layer: {"res": [7 floats],
-    "den5_median": float}} (max over the inputs)."""
+    values_differ metric of checksums.hpp:54-60), the max absolute Co5/So5 residual
+    |Co5-So5| and the median of max(|Co5|,|So5|,1) over positions (the CoC-D
+    denominator).  Returns {layer: {"res": [7 floats], "abs5": float, "den5_median":
+    float}} (max over the inputs)."""
     import torch
     from .ftconv import input_checksums, output_checksums, output_summations
     pn = ProtectedNet(net, batch, weight_seed, dev)
@@ -492,9 +499,11 @@ def layer_residuals(net, batch, weight_seed, dev, inputs):
                     den = torch.clamp(torch.maximum(c.abs(), sm.abs()), min=1.0)
                     res.append(float(((c - sm).abs() / den).max()))
                 den5 = torch.clamp(torch.maximum(cs[4].abs(), so[4].abs()), min=1.0)
-                rec = out.setdefault(op.dst, {"res": [0.0] * 7, "den5_median": 0.0})
+                abs5 = float((cs[4] - so[4]).abs().max())
+                rec = out.setdefault(op.dst, {"res": [0.0] * 7, "den5_median": 0.0, "abs5": 0.0})
                 rec["res"] = [max(a, b_) for a, b_ in zip(rec["res"], res)]
                 rec["den5_median"] = max(rec["den5_median"], float(den5.median()))
+                rec["abs5"] = max(rec["abs5"], abs5)
         torch.cuda.synchronize()
     finally:
         pn.close()
@@ -508,17 +517,24 @@ def taus_from_residuals(res, policy="detection", factor=4.0):
       families, rounded up to a power of ten -- no family false-flags, so CoC/RC/ClC
       corrections verify; the CoC-D floor is coarse (the m/n-weighted families carry
       the largest FP32-output noise).
-    * "detection": factor x the Co5/So5 residual alone, rounded up in the 1-2-5 series --
-      the finest floor at which fault-free CoC-D stays clean; the weighted families may
-      then fail the verifier, so correction falls over to the reference's own recompute
-      stage (workflow.hpp:325-338).
+    * "detection": factor x the ABSOLUTE Co5/So5 residual max|Co5-So5|, rounded up in
+      the 1-2-5 series.  He-normal kernels make Sum_{n,m} O nearly cancel at some
+      positions, where the comparator's denominator max(|c|,|s|,1) falls to its floor 1
+      and the relative residual becomes the absolute one; which positions cancel varies
+      with the input, so the relative maximum of a calibration input under-estimates
+      another input's (measured on VGG c11: 2e-5 calibrated, 3e-4 on the bench input).
+      The absolute residual bounds the relative one at every position for inputs of the
+      same scale.  This is the finest floor at which fault-free CoC-D stays clean; the
+      weighted families may then fail the verifier, so correction falls over to the
+      reference's own recompute stage (workflow.hpp:325-338).
     The same tau goes to the device and the oracle, so verdict parity is policy-free."""
     taus = {}
     for k, r in res.items():
+        t_all = 10.0 ** math.ceil(math.log10(max(max(r["res"]) * factor, 1e-7)))
         if policy == "all-families":
-            taus[k] = 10.0 ** math.ceil(math.log10(max(max(r["res"]) * factor, 1e-7)))
+            taus[k] = t_all
         elif policy == "detection":
-            taus[k] = _round_up_125(max(r["res"][4] * factor, 1e-7))
+            taus[k] = min(t_all, _round_up_125(max(max(r["abs5"], r["res"][4]) * factor, 1e-7)))
         else:
             raise ValueError(f"unknown tau policy {policy!r}")
     return taus
@@ -669,14 +685,15 @@ class BenchNet:
                 if name not in plan:
                     fp += int(rep.detected)
                     continue
-                stages[rep.stage] = stages.get(rep.stage, 0) + 1
+                key = "integrity_error" if rep.integrity_error else rep.stage
+                stages[key] = stages.get(key, 0) + 1
                 det += int(rep.detected)
                 for (_, _, _, _, bit) in plan[name]:
                     inj += 1
                     b = by_bit.setdefault(str(bit), [0, 0])
                     b[0] += int(rep.detected)
                     b[1] += 1
-            if all(reps[k].stage in REPAIRED for k in plan):
+            if all(reps[k].stage in REPAIRED and not reps[k].integrity_error for k in plan):
                 repaired_runs += 1
                 equal_runs += int(same)
         return {"policy": self.policy, "runs": runs, "faulted_layers": sum(stages.values()),

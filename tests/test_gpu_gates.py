@@ -1,0 +1,236 @@
+"""Device analogues of the reference's own gate tests.
+
+* C3 (proj/tests/acceptance.cpp:180-205): a 1000-entry campaign() corpus over the
+  acceptance toy model, replayed on the device: 0 missed detections, 0 failed
+  recoveries, > 500 asserted entries.  The reference runs it at T=double; the device
+  engine is FP32, so the toy model runs in FP32 at the reference's FP32 default
+  tau (workflow.hpp:19, 1e-4).
+* C4 (acceptance.cpp:207-320): every non-benign above-threshold entry corrected by
+  each scheme in isolation (Co5-only verifier): the ordering coc <= rc <= fc and
+  coc <= clc <= fc holds with strictness witnesses, and each isolated status equals
+  the oracle's or_isolated_scheme on the same FP32 output.
+* No false positives over 2000 random tiny FP32 layers (proj/tests/test_workflow.cpp:
+  218-234), with the reference's own seeds (mt19937_64(9000)).
+* C8 (acceptance.cpp:508-589): the detection overhead fraction falls as M grows.
+"""
+import numpy as np
+import pytest
+
+import oracle_py as O
+from paper_2003_12203_b200 import synth
+
+TOY = """{
+  "name": "toy",
+  "element_type": "f32",
+  "layers": [
+    {"name": "c1", "batch": 4, "channels": 3, "height": 12, "kernels": 6, "kernel_size": 3},
+    {"name": "c2", "batch": 4, "channels": 6, "height": 10, "kernels": 8, "kernel_size": 3, "bias": true},
+    {"name": "c3", "batch": 4, "channels": 8, "height": 8, "kernels": 4, "kernel_size": 3}
+  ]
+}"""
+
+
+class MT19937_64:
+    """std::mt19937_64 raw output (test helper: the reference's test seeds)."""
+    NN, MM = 312, 156
+    MATRIX_A = 0xB5026F5AA96619E9
+    UM, LM = 0xFFFFFFFF80000000, 0x7FFFFFFF
+    MASK = (1 << 64) - 1
+
+    def __init__(self, seed):
+        self.mt = [0] * self.NN
+        self.mt[0] = seed & self.MASK
+        for i in range(1, self.NN):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self.MASK
+        self.mti = self.NN
+
+    def __call__(self):
+        if self.mti >= self.NN:
+            mt = self.mt
+            for i in range(self.NN):
+                x = (mt[i] & self.UM) | (mt[(i + 1) % self.NN] & self.LM)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= self.MATRIX_A
+                mt[i] = mt[(i + self.MM) % self.NN] ^ xa
+            self.mti = 0
+        x = self.mt[self.mti]
+        self.mti += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & self.MASK
+
+
+def test_mt19937_64_known_answer():
+    # the C++ standard's check: the 10000th output of a default-seeded mt19937_64
+    g = MT19937_64(5489)
+    for _ in range(9999):
+        g()
+    assert g() == 9981545732273789042
+
+
+def _toy():
+    import torch
+    from paper_2003_12203_b200 import model_io as MI
+    import paper_2003_12203_b200 as F
+    cfg = MI.parse_model_config(TOY)
+    model = MI.build_model(cfg, MI.random_weights(cfg, 2024))
+    D0 = torch.from_numpy(MI.random_input(cfg.layers[0], 555)).cuda()
+    plans = [F.LayerPlan(rc_enabled=True, clc_enabled=True, tau=model.tau) for _ in cfg.layers]
+    return cfg, model, D0, plans
+
+
+_CORPUS = {}
+
+
+def _corpus_run():
+    if "run" not in _CORPUS:
+        from paper_2003_12203_b200 import campaign as K
+        cfg, model, D0, plans = _toy()
+        corpus = K.campaign(model.grids(), 1000, seed=4242)
+        _CORPUS["run"] = (cfg, model, D0, plans, corpus)
+    return _CORPUS["run"]
+
+
+@pytest.mark.gpu
+def test_c3_corpus_1000_entries_fp32():
+    import time
+    from paper_2003_12203_b200 import campaign as K
+    cfg, model, D0, plans, corpus = _corpus_run()
+    clean = model.clean_chain(D0)
+    t0 = time.perf_counter()
+    missed = failed = asserted = 0
+    above = []
+    for e in corpus:
+        r = K.replay_entry(model, D0, clean, e, plans)
+        above.append(r.above_threshold)
+        if r.above_threshold and not r.rep.detected:
+            missed += 1
+        if r.asserted:
+            asserted += 1
+            if not r.recovered:
+                failed += 1
+        if r.integrity_fatal:
+            failed += 1
+    elapsed = time.perf_counter() - t0
+    _CORPUS["above"] = above
+    print(f"C3 device: {asserted} asserted, {missed} missed, {failed} failed recoveries, {elapsed:.1f}s")
+    assert missed == 0 and failed == 0 and asserted > 500 and elapsed < 300.0, (asserted, missed, failed)
+
+
+@pytest.mark.gpu
+def test_c4_isolation_ordering_and_oracle_parity():
+    import torch
+    from paper_2003_12203_b200 import campaign as K
+    cfg, model, D0, plans, corpus = _corpus_run()
+    if "above" not in _CORPUS:
+        test_c3_corpus_1000_entries_fp32()
+    above = _CORPUS["above"]
+    clean = model.clean_chain(D0)
+    considered = violations = 0
+    rc_only = clc_only = fc_over_rc = fc_over_clc = 0
+    parity_checked = 0
+    for idx, e in enumerate(corpus):
+        if e.truth.benign or not above[idx]:
+            continue
+        if e.truth.expected_stage in ("discard", "reload"):
+            continue
+        considered += 1
+        Li = e.fault.layer_index
+        L = model.layers[Li]
+        Din = D0 if Li == 0 else clean[Li - 1]
+        Ocl = clean[Li]
+        faults = e.fault.device_faults()
+        ok = {}
+        for scheme in ("coc", "rc", "clc", "fc"):
+            Og, status, rep = L.isolated(Din, plans[Li], scheme, faults)
+            ok[scheme] = status == "corrected" and K.outputs_close(Og, Ocl)
+            if parity_checked < 120 and e.fault.target not in ("fmap", "kernel", "checksum"):
+                # same FP32 output on both sides: the oracle's isolated scheme
+                Of = K._faulted_output(L, Din, faults).cpu().numpy()
+                N, Ch, H, M, R = model.shapes[Li]
+                p = model.params[Li]
+                d = O.dims(N, Ch, H, M, R, p.stride, p.pad, p.groups, p.bias_enabled)
+                W = L._W
+                ref = O.isolated_scheme(d, Din.cpu().numpy(), W, L._bias, plans[Li].tau, Of, scheme)
+                assert status == ref["status"], (idx, scheme, status, ref)
+                if status == "corrected":
+                    assert sorted(rep.corrected_blocks) == sorted(ref["blocks"]), (idx, scheme, rep, ref)
+                parity_checked += 1
+        sc, sr, sl, sf = ok["coc"], ok["rc"], ok["clc"], ok["fc"]
+        if (sc and not sr) or (sr and not sf) or (sc and not sl) or (sl and not sf):
+            violations += 1
+        rc_only += sr and not sc
+        clc_only += sl and not sc
+        fc_over_rc += sf and not sr
+        fc_over_clc += sf and not sl
+    torch.cuda.synchronize()
+    print(f"C4 device: {considered} entries, {violations} violations; witnesses rc/clc/fc: "
+          f"{rc_only}/{clc_only}/{fc_over_rc}+{fc_over_clc}; oracle parity {parity_checked}")
+    assert considered > 300 and violations == 0
+    assert rc_only > 0 and clc_only > 0 and fc_over_rc > 0 and fc_over_clc > 0
+    assert parity_checked >= 100
+
+
+@pytest.mark.gpu
+def test_no_false_positives_2000_tiny_fp32_layers():
+    """proj/tests/test_workflow.cpp:218-234 on the device: same seeds, same shapes, FP32,
+    tau 1e-4, default ConvParams -- zero detections."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import model_io as MI
+    rng = MT19937_64(9000)
+    detections = 0
+    for rep in range(2000):
+        N = 1 + rng() % 3
+        M = 1 + rng() % 3
+        Ch = 1 + rng() % 2
+        R = 1 + rng() % 2
+        H = R + 1 + rng() % 4
+        D = MI.mt64_uniform(rng(), N * Ch * H * H).astype(np.float32).reshape(N, Ch, H, H)
+        W = MI.mt64_uniform(rng(), M * Ch * R * R).astype(np.float32).reshape(M, Ch, R, R)
+        L = F.ProtectedConv(W, None, F.ConvParams(), N, H)
+        _, r = L.protected(torch.from_numpy(D).cuda(), F.LayerPlan(rc_enabled=True, clc_enabled=False, tau=1e-4))
+        detections += int(r.detected)
+        L.close()
+    assert detections == 0
+
+
+@pytest.mark.gpu
+def test_c8_detection_overhead_falls_with_m():
+    """acceptance.cpp:508-589 on the device: N=8, Ch=64, H=56, 3x3 -- the clean-path
+    ABFT overhead fraction (protected vs unprotected conv, CUDA events, median of 15)
+    is smaller at M=64 than at M=8."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import model_io as MI
+    N, Ch, H, R = 8, 64, 56, 3
+    frac = {}
+    D = torch.from_numpy(MI.mt64_uniform(81, N * Ch * H * H).astype(np.float32).reshape(N, Ch, H, H)).cuda()
+    for M in (8, 64):
+        W = MI.mt64_uniform(82, M * Ch * R * R).astype(np.float32).reshape(M, Ch, R, R)
+        L = F.ProtectedConv(W, None, F.ConvParams(), N, H)
+        O_ = torch.empty(L.out_shape, device="cuda")
+        plan = F.LayerPlan(rc_enabled=False, clc_enabled=False, tau=1e-4)
+
+        def t(fn):
+            ts = []
+            for _ in range(15):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return sorted(ts)[7]
+        for _ in range(3):
+            L.conv_forward(D, O_)
+            L.protected(D, plan, O=O_)
+        tu = t(lambda: L.conv_forward(D, O_))
+        tp = t(lambda: L.protected(D, plan, O=O_))
+        frac[M] = (tp - tu) / tu
+        L.close()
+    print("C8 device overhead fraction", frac)
+    assert frac[64] < frac[8], frac

@@ -206,3 +206,20 @@ def test_profile_layer_on_device():
     d1 = P.LayerDims.of(L1)
     assert pr1.rc_t0 == P.cost_model("coc", d1) + P.cost_model("fc", d1)
     L1.close()
+
+
+def test_tau_policies_from_residuals():
+    """nets.taus_from_residuals: all-families = 4x the worst family, power of ten;
+    detection = 4x the absolute Co5/So5 residual in the 1-2-5 series, never coarser
+    than all-families; floors = tau x median denominator."""
+    from paper_2003_12203_b200 import nets
+    res = {"a": {"res": [1e-5, 1e-5, 3e-3, 1e-4, 2e-6, 1e-4, 1e-4], "abs5": 4.9e-5, "den5_median": 30.0},
+           "b": {"res": [1e-6] * 7, "abs5": 0.5, "den5_median": 2.0}}
+    t_all = nets.taus_from_residuals(res, "all-families")
+    t_det = nets.taus_from_residuals(res, "detection")
+    assert t_all == {"a": 0.1, "b": 1e-5}
+    assert t_det["a"] == 2e-4 and t_det["b"] == 1e-5
+    fl = nets.detection_floor(res, t_det)
+    assert abs(fl["a"] - 2e-4 * 30.0) < 1e-12
+    with pytest.raises(ValueError):
+        nets.taus_from_residuals(res, "nope")
