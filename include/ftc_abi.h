@@ -347,6 +347,16 @@ int ftc_layer_kernel_time(ftc_layer* layer, double* conv_ms, int32_t* conv_launc
                           int32_t reset);
 uint64_t ftc_kernel_launches(void);
 
+/* ---------------------------------------------------------------- device memory
+ * For hosts that do not link the CUDA runtime themselves (the C++ wrappers in
+ * include/ftconv_b200/, a cgo/JNI/ctypes binding): device allocations and copies
+ * through the library's own runtime.  kind: 0 host->device, 1 device->host,
+ * 2 device->device; the copy is ordered on `stream` and complete on return. */
+int ftc_device_alloc(size_t bytes, void** ptr);
+int ftc_device_free(void* ptr);
+int ftc_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream);
+int ftc_memset_zero(void* dst, size_t bytes, void* stream);
+
 /* ---------------------------------------------------------------- building blocks
  * Device implementations of checksums.hpp / schemes.hpp primitives, FP64,
  * summed in the reference's association order (bitwise equal to the reference at

@@ -45,39 +45,59 @@ inline void check(int st, const char* what) {
   }
 }
 
-/// Dense NCHW host tensor (tensor.hpp:17-71), FP32 only: the device path is FP32.
-class Tensor4 {
+/// Dense NCHW host tensor (tensor.hpp:17-71).  The device path computes in FP32
+/// (Tensor4); the checksum building blocks return FP64 tensors (Tensor4d), the
+/// reference's T=double instantiation the verdicts are defined on.
+template <typename T>
+class BasicTensor4 {
  public:
-  Tensor4() : dims_{0, 0, 0, 0} {}
-  Tensor4(std::size_t d0, std::size_t d1, std::size_t d2, std::size_t d3)
-      : dims_{d0, d1, d2, d3}, data_(d0 * d1 * d2 * d3, 0.f) {}
+  BasicTensor4() : dims_{0, 0, 0, 0} {}
+  BasicTensor4(std::size_t d0, std::size_t d1, std::size_t d2, std::size_t d3)
+      : dims_{d0, d1, d2, d3}, data_(d0 * d1 * d2 * d3, T(0)) {}
   std::size_t dim(std::size_t i) const { return dims_[i]; }
   const std::array<std::size_t, 4>& dims() const { return dims_; }
   std::size_t size() const { return data_.size(); }
-  float& operator()(std::size_t a, std::size_t b, std::size_t c, std::size_t d) {
+  T& operator()(std::size_t a, std::size_t b, std::size_t c, std::size_t d) {
     return data_[((a * dims_[1] + b) * dims_[2] + c) * dims_[3] + d];
   }
-  float operator()(std::size_t a, std::size_t b, std::size_t c, std::size_t d) const {
+  T operator()(std::size_t a, std::size_t b, std::size_t c, std::size_t d) const {
     return data_[((a * dims_[1] + b) * dims_[2] + c) * dims_[3] + d];
   }
-  float* data() { return data_.data(); }
-  const float* data() const { return data_.data(); }
-  std::vector<float>& raw() { return data_; }
-  const std::vector<float>& raw() const { return data_; }
-  bool same_shape(const Tensor4& o) const { return dims_ == o.dims_; }
+  T* data() { return data_.data(); }
+  const T* data() const { return data_.data(); }
+  std::vector<T>& raw() { return data_; }
+  const std::vector<T>& raw() const { return data_; }
+  bool same_shape(const BasicTensor4& o) const { return dims_ == o.dims_; }
   /// Seeded uniform fill (same generator and cast as the reference's Tensor4::random).
-  static Tensor4 random(std::size_t d0, std::size_t d1, std::size_t d2, std::size_t d3,
-                        std::uint64_t seed, double lo = -1.0, double hi = 1.0) {
-    Tensor4 t(d0, d1, d2, d3);
+  static BasicTensor4 random(std::size_t d0, std::size_t d1, std::size_t d2, std::size_t d3,
+                             std::uint64_t seed, double lo = -1.0, double hi = 1.0) {
+    BasicTensor4 t(d0, d1, d2, d3);
     std::mt19937_64 rng(seed);
     std::uniform_real_distribution<double> dist(lo, hi);
-    for (float& v : t.data_) v = static_cast<float>(dist(rng));
+    for (T& v : t.data_) v = static_cast<T>(dist(rng));
     return t;
   }
 
  private:
   std::array<std::size_t, 4> dims_;
-  std::vector<float> data_;
+  std::vector<T> data_;
+};
+
+using Tensor4 = BasicTensor4<float>;
+using Tensor4d = BasicTensor4<double>;
+
+/// E x E row-major checksum/summation grid (tensor.hpp:74-89), FP64.
+struct Grid {
+  std::size_t n = 0;
+  std::vector<double> v;
+  Grid() = default;
+  explicit Grid(std::size_t side) : n(side), v(side * side, 0.0) {}
+  double& operator()(std::size_t x, std::size_t y) { return v[x * n + y]; }
+  double operator()(std::size_t x, std::size_t y) const { return v[x * n + y]; }
+  Grid& operator+=(const Grid& o) {
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] += o.v[i];
+    return *this;
+  }
 };
 
 struct ConvParams {

@@ -31,6 +31,7 @@ EXPORTS = (
     "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
     "ftc_conv_backward_host", "ftc_protected_backward_host", "ftc_isolated_scheme",
     "ftc_protected_conv_cancel", "ftc_layer_detect_record",
+    "ftc_device_alloc", "ftc_device_free", "ftc_memcpy", "ftc_memset_zero",
 )
 
 
@@ -168,6 +169,10 @@ def lib():
         L.ftc_glue_act_pool_cd1.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]
         L.ftc_protected_conv_launch_cd1.argtypes = [vp, C.POINTER(Plan), vp, vp, vp, C.POINTER(Fault), i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
+        L.ftc_device_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+        L.ftc_device_free.argtypes = [vp]
+        L.ftc_memcpy.argtypes = [vp, vp, C.c_size_t, i32, vp]
+        L.ftc_memset_zero.argtypes = [vp, C.c_size_t, vp]
         _lib = L
     return _lib
 

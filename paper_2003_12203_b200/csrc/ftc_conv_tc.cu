@@ -648,6 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
               mma_tf32_ts(d_corr, a_hi + k * 8u, desc_sw128(b_lo + k * 32u), idesc, 1u);
             }
           }
+          // the other issuer's next MMAs must enter the pipe after these: tcgen05 ops of
+          // different threads are ordered only through a fence::before/after_thread_sync
+          // pair around the synchronisation (without it a later half's MMA could
+          // accumulate first -- a run-to-run 1-ulp difference in the output)
+          tc_before();
           mbar_arrive(turn);
           TC_TRACE(mprof, 5, g);
           mma_commit(emptyA0 + 8 * hs);

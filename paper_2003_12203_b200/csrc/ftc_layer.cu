@@ -1320,6 +1320,39 @@ int ftc_protected_conv_host(ftc_layer* L, const ftc_plan* plan, const float* D_h
   return st;
 }
 
+// ------------------------------------------------------------------ device memory
+int ftc_device_alloc(size_t bytes, void** ptr) {
+  if (!ptr) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  *ptr = nullptr;
+  if (bytes == 0) return FTC_OK;
+  FTC_CUDA_CHECK(cudaMalloc(ptr, bytes));
+  return FTC_OK;
+}
+
+int ftc_device_free(void* ptr) {
+  if (ptr) FTC_CUDA_CHECK(cudaFree(ptr));
+  return FTC_OK;
+}
+
+int ftc_memcpy(void* dst, const void* src, size_t bytes, int32_t kind, void* stream) {
+  if (bytes == 0) return FTC_OK;
+  if (!dst || !src) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  static const cudaMemcpyKind kinds[3] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                          cudaMemcpyDeviceToDevice};
+  if (kind < 0 || kind > 2) RET_ERR(FTC_INVALID_ARGUMENT, "kind must be 0 (h2d), 1 (d2h) or 2 (d2d)");
+  cudaStream_t s = (cudaStream_t)stream;
+  FTC_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, kinds[kind], s));
+  FTC_CUDA_CHECK(cudaStreamSynchronize(s));
+  return FTC_OK;
+}
+
+int ftc_memset_zero(void* dst, size_t bytes, void* stream) {
+  if (bytes == 0) return FTC_OK;
+  if (!dst) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  FTC_CUDA_CHECK(cudaMemsetAsync(dst, 0, bytes, (cudaStream_t)stream));
+  return FTC_OK;
+}
+
 // ------------------------------------------------------------------ building blocks
 int ftc_input_checksums(const ftc_conv_desc* d, const float* D, double* cd1, double* cd2,
                         void* stream) {
