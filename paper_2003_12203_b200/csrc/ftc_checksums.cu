@@ -101,11 +101,17 @@ __global__ void k_kernel_checksums(const float* __restrict__ W, int M, int Ckw, 
   if (e >= per * groups) return;
   const int g = e / per, r = e % per, mpg = M / groups;
   double s1 = 0.0, s2 = 0.0;
-  for (int mg = 0; mg < mpg; ++mg) {
-    const int m = g * mpg + mg;
-    const double v = W[(long long)m * per + r];
-    s1 = dadd(s1, v);
-    s2 = dadd(s2, dmul((double)m, v));
+  for (int mg0 = 0; mg0 < mpg; mg0 += 8) {  // 8 loads in flight, then the ordered adds
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = mg0 + u < mpg ? (double)W[(long long)(g * mpg + mg0 + u) * per + r] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (mg0 + u < mpg) {
+        s1 = dadd(s1, v[u]);
+        s2 = dadd(s2, dmul((double)(g * mpg + mg0 + u), v[u]));
+      }
+    }
   }
   cw1[e] = s1;
   cw2[e] = s2;
@@ -194,10 +200,17 @@ __global__ void k_sum_cols(VirtualO v, int N, int M, int E2, uint32_t which, con
   if (q >= (long long)M * E2) return;
   const int m = (int)(q / E2), f = (int)(q % E2);
   double s1 = 0.0, s3 = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double x = vo(v, ((long long)n * M + m) * E2 + f);
-    s1 = dadd(s1, x);
-    s3 = dadd(s3, dmul((double)n, x));
+  for (int n0 = 0; n0 < N; n0 += 8) {  // 8 loads in flight, then the ordered adds
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = n0 + u < N ? vo(v, ((long long)(n0 + u) * M + m) * E2 + f) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (n0 + u < N) {
+        s1 = dadd(s1, x[u]);
+        s3 = dadd(s3, dmul((double)(n0 + u), x[u]));
+      }
+    }
   }
   if (bias) {
     const double b = bias[m];
@@ -215,10 +228,17 @@ __global__ void k_sum_rows(VirtualO v, int N, int M, int E2, uint32_t which, con
   if (q >= (long long)N * E2) return;
   const int n = (int)(q / E2), f = (int)(q % E2);
   double s2 = 0.0, s4 = 0.0;
-  for (int m = 0; m < M; ++m) {
-    const double x = vo(v, ((long long)n * M + m) * E2 + f);
-    s2 = dadd(s2, x);
-    s4 = dadd(s4, dmul((double)m, x));
+  for (int m0 = 0; m0 < M; m0 += 8) {  // 8 loads in flight, then the ordered adds
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = m0 + u < M ? vo(v, ((long long)n * M + m0 + u) * E2 + f) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (m0 + u < M) {
+        s2 = dadd(s2, x[u]);
+        s4 = dadd(s4, dmul((double)(m0 + u), x[u]));
+      }
+    }
   }
   if (agg) {
     s2 = dsub(s2, agg[0]);
@@ -228,26 +248,76 @@ __global__ void k_sum_rows(VirtualO v, int N, int M, int E2, uint32_t which, con
   if (which & FTC_CK_O4) so4[q] = s4;
 }
 
-// So5/So6/So7 with a warp per position (warp_seq_sums567): one thread per position
-// walking the N*M terms with dependent loads took ~10 ms per call on AlexNet's layers.
-__global__ void __launch_bounds__(256) k_sum_total_warp(VirtualO v, int N, int M, int E2, uint32_t which,
-                                                       const double* agg, double* so5, double* so6, double* so7) {
-  __shared__ double buf[8][2 * kSeqBatch];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (f >= E2) return;  // whole warps exit together
-  double s5, s6, s7;
-  warp_seq_sums567([&](long long q) { return vo(v, q * E2 + f); }, (long long)N * M, M, buf[w], s5, s6, s7);
-  if (lane != 0) return;
-  if (agg) {
-    const double nN = (double)N, wnn = (double)((long long)N * (N - 1) / 2);
-    s5 = dsub(s5, dmul(nN, agg[0]));
-    s6 = dsub(s6, dmul(nN, agg[1]));
-    s7 = dsub(s7, dmul(wnn, agg[0]));
+// So5/So6/So7 (checksums.hpp:176-189): for every position the (n, m) sequence, n outer,
+// m inner, summed strictly in order -- one chain of N*M dependent FP64 adds per position
+// and family (32768 at AlexNet conv2), so the kernel is bound by how fast a chain steps
+// (DADD latency 8.2 cycles on B200, tools/ubench_fp64.cu).  A warp owns one (position,
+// family): lane l loads term q = 32b + l of batch b and forms its product
+// y = w(q) * x(q) (exact: w = 1, m or n), and the chain walks the batch with shuffles,
+// s = dadd(s, y of lane u) for u = 0..31 -- two SHFL and one DADD per term, the shuffles
+// independent of s, so the chain runs at the add latency.  Batches are loaded three
+// ahead (registers).  The three families of a position are adjacent warps of one block
+// and share the position's sectors in L1.  (A warp per position with lane 0 adding from
+// shared memory took ~1 ms per call at conv2; a lane per position with a cp.async ring,
+// ~2 ms: the per-lane copy instructions, not the adds, set the pace,
+// tools/ubench_seq.cu.)
+constexpr int kSeqWarps = 3;  // warps per block: the three families of one position
+template <bool VIRT>
+__global__ void __launch_bounds__(32 * kSeqWarps) k_seq_sums567(VirtualO v, int N, int M, int E2,
+                                                                const int* __restrict__ list,
+                                                                const int* __restrict__ count, const double* agg,
+                                                                double* __restrict__ so5, double* __restrict__ so6,
+                                                                double* __restrict__ so7, int dbg) {
+  (void)dbg;
+  const int lane = threadIdx.x & 31, fam = threadIdx.x >> 5;
+  const int p = blockIdx.x;
+  const int npos = list ? *count : E2;
+  if (p >= npos) return;
+  double* out = fam == 0 ? so5 : fam == 1 ? so6 : so7;
+  if (!out) return;  // whole warp
+  const int f = list ? list[p] : p;
+  const long long NM = (long long)N * M;
+  const long long nb = (NM + 31) / 32;
+  // this lane's term of batch b, weighted (exact product); terms past the end are +0.0,
+  // which leaves a sum that started at +0.0 unchanged
+  auto term = [&](long long b) -> double {
+    const long long q = b * 32 + lane;
+    if (q >= NM) return 0.0;
+    const long long idx = q * E2 + f;
+    double x = (double)__ldg(v.O + idx);
+    if (VIRT && __ldg(v.present + idx)) x = __ldg(v.ov + idx);
+    if (fam == 0) return x;
+    const int n = (int)(q / M), m = (int)(q - (long long)n * M);
+    return dmul((double)(fam == 1 ? m : n), x);
+  };
+  double s = 0.0;
+  auto walk = [&](double y) {
+    double t[32];  // all of the batch's shuffles first, then the 32 dependent adds
+#pragma unroll
+    for (int u = 0; u < 32; ++u) t[u] = __shfl_sync(0xffffffffu, y, u);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) s = dadd(s, t[u]);
+  };
+  double ya = term(0), yb = term(1), yc = term(2);
+  for (long long b = 0; b < nb; b += 3) {
+    const double y0 = ya;
+    ya = term(b + 3);
+    walk(y0);
+    if (b + 1 >= nb) break;
+    const double y1 = yb;
+    yb = term(b + 4);
+    walk(y1);
+    if (b + 2 >= nb) break;
+    const double y2 = yc;
+    yc = term(b + 5);
+    walk(y2);
   }
-  if (which & FTC_CK_O5) so5[f] = s5;
-  if (which & FTC_CK_O6) so6[f] = s6;
-  if (which & FTC_CK_O7) so7[f] = s7;
+  if (lane != 0) return;
+  if (agg) {  // BiasAdjuster (checksums.hpp:226-235)
+    const double nN = (double)N, wnn = (double)((long long)N * (N - 1) / 2);
+    s = dsub(s, fam == 0 ? dmul(nN, agg[0]) : fam == 1 ? dmul(nN, agg[1]) : dmul(wnn, agg[0]));
+  }
+  out[f] = s;
 }
 
 // ------------------------------------------------------------------ K6: CoC-D
@@ -647,6 +717,17 @@ int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s
   return FTC_OK;
 }
 
+int launch_seq_sums567(const VirtualO& v, int N, int M, int E2, const int* list, const int* count, const double* agg,
+                       double* so5, double* so6, double* so7, cudaStream_t s) {
+  const dim3 g((unsigned)E2);
+  if (v.present)
+    FTC_LAUNCH(k_seq_sums567<true><<<g, 32 * kSeqWarps, 0, s>>>(v, N, M, E2, list, count, agg, so5, so6, so7, 0));
+  else
+    FTC_LAUNCH(k_seq_sums567<false><<<g, 32 * kSeqWarps, 0, s>>>(v, N, M, E2, list, count, agg, so5, so6, so7, 0));
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
 int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t which,
                              const float* bias, const double* agg, double* const so[7],
                              cudaStream_t s) {
@@ -659,8 +740,9 @@ int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t wh
                                                                    bias ? agg : nullptr, so[1],
                                                                    so[3]));
   if (which & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7))
-    FTC_LAUNCH(k_sum_total_warp<<<blocks_for((long long)E2 * 32), kThreads, 0, s>>>(
-        v, N, M, E2, which, bias ? agg : nullptr, so[4], so[5], so[6]));
+    if (const int st_ = launch_seq_sums567(v, N, M, E2, nullptr, nullptr, bias ? agg : nullptr, (which & FTC_CK_O5) ? so[4] : nullptr,
+                          (which & FTC_CK_O6) ? so[5] : nullptr, (which & FTC_CK_O7) ? so[6] : nullptr, s))
+      return st_;
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

@@ -166,71 +166,6 @@ struct DetectStats {
   unsigned long long max_rel_dev_bits;
 };
 
-// Clean-path CoC-D fused into the tcgen05 conv (TMA im2col engine): Co5 = Cd1 (x) Cw1 is
-// computed before the conv; the conv adds its pixels' row sums into So5 (FP64 atomics)
-// and its last CTA compares them and publishes the record.
-// So5/So6/So7 of output position f in the reference's association order (checksums.hpp:
-// 224-229: n ascending, then m ascending, one double accumulator each) with a whole warp:
-// the lanes stage the next kSeqBatch terms of the (n, m) sequence in shared memory (any
-// load order) while lane 0 adds the current batch strictly in sequence.  `buf` is this
-// warp's 2 * kSeqBatch doubles of shared memory.  Returns the sums in lane 0.
-constexpr int kSeqBatch = 256;
-template <typename Load>
-__device__ __forceinline__ void warp_seq_sums567(Load load, long long NM, int M, double* buf, double& s5, double& s6,
-                                                 double& s7) {
-  const int lane = threadIdx.x & 31;
-  s5 = s6 = s7 = 0.0;
-  auto stage = [&](long long q0, int b) {
-#pragma unroll
-    for (int u = 0; u < kSeqBatch / 32; ++u) {
-      const long long q = q0 + u * 32 + lane;
-      buf[b * kSeqBatch + u * 32 + lane] = q < NM ? load(q) : 0.0;
-    }
-  };
-  stage(0, 0);
-  __syncwarp();
-  int b = 0;
-  for (long long q0 = 0; q0 < NM; q0 += kSeqBatch, b ^= 1) {
-    if (q0 + kSeqBatch < NM) stage(q0 + kSeqBatch, b ^ 1);  // next batch in flight
-    if (lane == 0) {
-      const int cnt = (int)min((long long)kSeqBatch, NM - q0);
-      int n = (int)(q0 / M), m = (int)(q0 - (q0 / M) * M);
-      double dn = (double)n, dm = (double)m;
-      const double dM = (double)M;
-      const double* x = buf + b * kSeqBatch;
-      int i = 0;
-      // 8 terms per step: their shared-memory loads issue together, the adds stay in order
-      for (; i + 8 <= cnt; i += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = x[i + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          s5 = dadd(s5, v[u]);
-          s6 = dadd(s6, dmul(dm, v[u]));
-          s7 = dadd(s7, dmul(dn, v[u]));
-          dm += 1.0;
-          if (dm == dM) {
-            dm = 0.0;
-            dn += 1.0;
-          }
-        }
-      }
-      for (; i < cnt; ++i) {
-        s5 = dadd(s5, x[i]);
-        s6 = dadd(s6, dmul(dm, x[i]));
-        s7 = dadd(s7, dmul(dn, x[i]));
-        dm += 1.0;
-        if (dm == dM) {
-          dm = 0.0;
-          dn += 1.0;
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
 struct Co5Tap {  // one (c, i, j) term of Co5 = Cd1 (*) Cw1
   int off;         // c*H*H + i*H + j
   short i, j;
@@ -312,6 +247,10 @@ struct VirtualO {  // FP32 O plus FP64 overrides left by the verifier's rollback
   const double* ov;        // N*M*E2 or null
   const uint8_t* present;  // N*M*E2 or null
 };
+// So5/So6/So7 in the reference's (n, m) order for the positions in list[0 : *count]
+// (list == null: all E2 positions), written at their positions; agg: bias aggregates or null
+int launch_seq_sums567(const VirtualO& v, int N, int M, int E2, const int* list, const int* count, const double* agg,
+                       double* so5, double* so6, double* so7, cudaStream_t s);
 // output_summations + BiasAdjuster (exact order)
 int launch_output_summations(const VirtualO& v, int N, int M, int E, uint32_t which,
                              const float* bias, const double* agg, double* const so[7],
@@ -398,6 +337,9 @@ struct VerifyWS {
   uint8_t* present;
   uint8_t* touched5;  // E2
   uint8_t* touched1;  // M*E2
+  double* fresh;      // 3*E2: fresh So5/So6/So7 of the touched positions
+  int* tlist;         // E2: the touched positions
+  int* tcount;        // 1
 };
 // workflow.hpp:205-219 verifier emulated over the patch list (see ftc_schemes.cu)
 int run_verify(const Fam& F, unsigned trusted, const float* O, int N, int M, int E2, int bias,

@@ -101,6 +101,9 @@ struct ftc_layer {
   double* ov = nullptr;
   uint8_t* present = nullptr;
   uint8_t* touched5 = nullptr;
+  double* fresh567 = nullptr;  // verifier: fresh So5/So6/So7 of the touched positions
+  int* tlist = nullptr;
+  int* tcount = nullptr;
   uint8_t* touched1 = nullptr;
   Patches patches{};
   SchemeResult* res = nullptr;
@@ -245,6 +248,9 @@ int alloc_error_path(ftc_layer* L) {
   CK(dalloc(&L->present, L->nO));
   CK(dalloc(&L->touched5, E2));
   CK(dalloc(&L->touched1, (size_t)M * E2));
+  CK(dalloc(&L->fresh567, 3 * (size_t)E2));
+  CK(dalloc(&L->tlist, E2));
+  CK(dalloc(&L->tcount, 1));
   FTC_CUDA_CHECK(cudaMemset(L->present, 0, L->nO));
   FTC_CUDA_CHECK(cudaMemset(L->touched5, 0, E2));
   FTC_CUDA_CHECK(cudaMemset(L->touched1, 0, (size_t)M * E2));
@@ -281,7 +287,7 @@ void free_layer(ftc_layer* L) {
     F(L->s[k]);
   }
   F(L->tmp_c); F(L->tmp_s); F(L->tmp_cw1); F(L->tmp_cw2); F(L->ov); F(L->present); F(L->touched5);
-  F(L->touched1); F(L->patches.n); F(L->patches.m); F(L->patches.f); F(L->patches.d); F(L->res);
+  F(L->touched1); F(L->fresh567); F(L->tlist); F(L->tcount); F(L->patches.n); F(L->patches.m); F(L->patches.f); F(L->patches.d); F(L->res);
   F(L->colmask); F(L->rowmask); F(L->colany); F(L->rowany); F(L->plane_mask); F(L->iscratch);
   if (L->stats_h) cudaFreeHost(L->stats_h);
   if (L->fstats_h) cudaFreeHost(L->fstats_h);
@@ -454,7 +460,7 @@ int probe(EP& e, bool row0, bool* consistent) {
 int verify_patches(EP& e, int np, bool* pass) {
   ftc_layer* L = e.L;
   const unsigned trusted = e.cs_have & e.trust_mask;
-  VerifyWS ws{L->ov, L->present, L->touched5, L->touched1};
+  VerifyWS ws{L->ov, L->present, L->touched5, L->touched1, L->fresh567, L->tlist, L->tcount};
   CK(run_verify(fam(e), trusted, L->O, L->d.N, L->d.M, L->E2, L->d.bias_enabled, L->bias, L->agg,
                 L->plan.tau, L->patches, L->res, np, ws, L->iscratch, e.s));
   e.ov_dirty = true;

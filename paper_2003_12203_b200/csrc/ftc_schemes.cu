@@ -296,36 +296,25 @@ __global__ void k_verify_apply(Patches p, int np, int M, int E2, const float* O,
   }
 }
 
-// fresh So5/So6/So7 where touched, cached elsewhere; compare (workflow.hpp:209-211).
-// A warp per position: touched positions re-sum the (n, m) sequence with
-// warp_seq_sums567 (a thread walking N*M dependent loads made each verify ~18 ms).
-__global__ void __launch_bounds__(256) k_verify_pos(Fam F, unsigned trusted, const float* O, int N, int M, int E2,
-                                                   int bias, const double* agg, double tau, VerifyWS ws,
-                                                   int32_t* fail) {
-  __shared__ double buf[8][2 * kSeqBatch];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (f >= E2) return;  // whole warps exit together
-  double s5, s6, s7;
-  if (ws.touched5[f]) {
-    warp_seq_sums567([&](long long q) { return vo(O, ws.ov, ws.present, q * E2 + f); }, (long long)N * M, M,
-                     buf[w], s5, s6, s7);
-    if (bias) {
-      const double nN = (double)N, wn = (double)((long long)N * (N - 1) / 2);
-      s5 = dsub(s5, dmul(nN, agg[0]));
-      s6 = dsub(s6, dmul(nN, agg[1]));
-      s7 = dsub(s7, dmul(wn, agg[0]));
-    }
-  } else {
-    s5 = (trusted & FTC_CK_O5) ? F.s[4][f] : 0.0;
-    s6 = (trusted & FTC_CK_O6) ? F.s[5][f] : 0.0;
-    s7 = (trusted & FTC_CK_O7) ? F.s[6][f] : 0.0;
-  }
-  if (lane != 0) return;
+// the positions a patch touched (their So5/So6/So7 are re-summed fresh)
+__global__ void k_touched_list(const uint8_t* __restrict__ touched5, int E2, int* list, int* count) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < E2 && touched5[f]) list[atomicAdd(count, 1)] = f;
+}
+
+// fresh So5/So6/So7 where touched (launch_seq_sums567 over the touched list, reference
+// order), cached elsewhere; compare (workflow.hpp:209-211)
+__global__ void k_verify_pos(Fam F, unsigned trusted, int E2, double tau, VerifyWS ws, int32_t* fail) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= E2) return;
+  const bool t = ws.touched5[f];
   bool bad = false;
-  if ((trusted & FTC_CK_O5) && values_differ(F.c[4][f], s5, tau)) bad = true;
-  if ((trusted & FTC_CK_O6) && values_differ(F.c[5][f], s6, tau)) bad = true;
-  if ((trusted & FTC_CK_O7) && values_differ(F.c[6][f], s7, tau)) bad = true;
+  for (int k = 0; k < 3; ++k) {
+    const unsigned bit = FTC_CK_O5 << k;
+    if (!(trusted & bit)) continue;
+    const double sv = t ? ws.fresh[(long long)k * E2 + f] : F.s[4 + k][f];
+    if (values_differ(F.c[4 + k][f], sv, tau)) bad = true;
+  }
   if (bad) *fail = 1;
 }
 
@@ -338,10 +327,17 @@ __global__ void k_verify_col(Fam F, unsigned trusted, const float* O, const floa
   if (ws.touched1[q]) {
     const int m = (int)(q / E2), f = (int)(q % E2);
     s1 = s3 = 0.0;
-    for (int n = 0; n < N; ++n) {
-      const double x = vo(O, ws.ov, ws.present, ((long long)n * M + m) * E2 + f);
-      s1 = dadd(s1, x);
-      s3 = dadd(s3, dmul((double)n, x));
+    for (int n0 = 0; n0 < N; n0 += 8) {  // 8 loads in flight, then the ordered adds
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = n0 + u < N ? vo(O, ws.ov, ws.present, ((long long)(n0 + u) * M + m) * E2 + f) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (n0 + u < N) {
+          s1 = dadd(s1, x[u]);
+          s3 = dadd(s3, dmul((double)(n0 + u), x[u]));
+        }
+      }
     }
     if (bias_dev) {
       const double b = bias_dev[m];
@@ -469,8 +465,17 @@ int run_verify(const Fam& F, unsigned trusted, const float* O, int N, int M, int
     k_verify_apply<<<grid_for(np), kT, 0, s>>>(p, np, M, E2, O, ws);
     count_launch();
   }
-  if (trusted & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7))
-    FTC_LAUNCH(k_verify_pos<<<(E2 + 7) / 8, 256, 0, s>>>(F, trusted, O, N, M, E2, bias, agg, tau, ws, fail));
+  if (trusted & (FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7)) {
+    FTC_CUDA_CHECK(cudaMemsetAsync(ws.tcount, 0, sizeof(int), s));
+    FTC_LAUNCH(k_touched_list<<<grid_for(E2), kT, 0, s>>>(ws.touched5, E2, ws.tlist, ws.tcount));
+    const VirtualO v{O, ws.ov, ws.present};
+    if (const int st_ = launch_seq_sums567(v, N, M, E2, ws.tlist, ws.tcount, bias ? agg : nullptr,
+                          (trusted & FTC_CK_O5) ? ws.fresh : nullptr,
+                          (trusted & FTC_CK_O6) ? ws.fresh + E2 : nullptr,
+                          (trusted & FTC_CK_O7) ? ws.fresh + 2 * (long long)E2 : nullptr, s))
+      return st_;
+    FTC_LAUNCH(k_verify_pos<<<grid_for(E2), kT, 0, s>>>(F, trusted, E2, tau, ws, fail));
+  }
   if (trusted & (FTC_CK_O1 | FTC_CK_O3))
     FTC_LAUNCH(k_verify_col<<<(int)(((long long)M * E2 + kT - 1) / kT), kT, 0, s>>>(
         F, trusted, O, bias ? bias_dev : nullptr, N, M, E2, tau, ws, fail));
