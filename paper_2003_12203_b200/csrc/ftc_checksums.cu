@@ -120,10 +120,18 @@ __global__ void k_kernel_checksums(const float* __restrict__ W, int M, int Ckw, 
 // ------------------------------------------------------------------ K4: exact FP64 conv
 // conv_direct (conv.hpp:39-62) at T=double: one thread per output, (k,i,j) ascending,
 // padded taps contribute 0*w exactly like padded_at (:28-37).
+template <typename TI, typename TW>
+struct ExactJobs {  // up to three independent convolutions in one launch (blockIdx.y)
+  const TI* in[3];
+  const TW* w[3];
+  double* out[3];
+};
 template <typename TI, typename TW, int RT>
-__global__ void k_conv_f64_exact(const TI* __restrict__ in, const TW* __restrict__ w,
-                                 double* __restrict__ out, int B, int Cin, int H, int Mo, int Ckw,
-                                 int Rrt, int U, int pad, int groups, int E) {
+__global__ void k_conv_f64_exact(ExactJobs<TI, TW> jobs, int B, int Cin, int H, int Mo, int Ckw, int Rrt, int U,
+                                 int pad, int groups, int E) {
+  const TI* __restrict__ in = jobs.in[blockIdx.y];
+  const TW* __restrict__ w = jobs.w[blockIdx.y];
+  double* __restrict__ out = jobs.out[blockIdx.y];
   const int R = RT > 0 ? RT : Rrt;
   const long long total = (long long)B * Mo * E * E;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -684,13 +692,14 @@ int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, d
 }
 
 template <typename TI, typename TW>
-void conv_f64_exact_dispatch(const TI* in, const TW* w, double* out, int B, int Cin, int H, int Mo, int Ckw, int R,
+void conv_f64_exact_dispatch(const ExactJobs<TI, TW>& j, int nj, int B, int Cin, int H, int Mo, int Ckw, int R,
                              int U, int pad, int groups, int E, int g, cudaStream_t s) {
+  const dim3 grid((unsigned)g, (unsigned)nj);
   switch (R) {
-    case 1: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 1><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
-    case 3: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 3><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
-    case 5: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 5><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
-    default: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 0><<<g, 128, 0, s>>>(in, w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    case 1: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 1><<<grid, 128, 0, s>>>(j, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    case 3: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 3><<<grid, 128, 0, s>>>(j, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    case 5: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 5><<<grid, 128, 0, s>>>(j, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
+    default: FTC_LAUNCH(k_conv_f64_exact<TI, TW, 0><<<grid, 128, 0, s>>>(j, B, Cin, H, Mo, Ckw, R, U, pad, groups, E)); break;
   }
 }
 
@@ -700,13 +709,30 @@ int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64
   const long long total = (long long)B * Mo * E * E;
   const int g = blocks_for(total, 128);
   if (in_f64 && w_f64)
-    conv_f64_exact_dispatch((const double*)in, (const double*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
+    conv_f64_exact_dispatch(ExactJobs<double, double>{{(const double*)in}, {(const double*)w}, {out}}, 1, B, Cin, H,
+                            Mo, Ckw, R, U, pad, groups, E, g, s);
   else if (in_f64)
-    conv_f64_exact_dispatch((const double*)in, (const float*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
+    conv_f64_exact_dispatch(ExactJobs<double, float>{{(const double*)in}, {(const float*)w}, {out}}, 1, B, Cin, H, Mo,
+                            Ckw, R, U, pad, groups, E, g, s);
   else if (w_f64)
-    conv_f64_exact_dispatch((const float*)in, (const double*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
+    conv_f64_exact_dispatch(ExactJobs<float, double>{{(const float*)in}, {(const double*)w}, {out}}, 1, B, Cin, H, Mo,
+                            Ckw, R, U, pad, groups, E, g, s);
   else
-    conv_f64_exact_dispatch((const float*)in, (const float*)w, out, B, Cin, H, Mo, Ckw, R, U, pad, groups, E, g, s);
+    conv_f64_exact_dispatch(ExactJobs<float, float>{{(const float*)in}, {(const float*)w}, {out}}, 1, B, Cin, H, Mo,
+                            Ckw, R, U, pad, groups, E, g, s);
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+int launch_conv_block3(const double* const in[3], const double* const w[3], double* const out[3], int nj, int Cin,
+                       int H, int R, int U, int pad, int E, cudaStream_t s) {
+  ExactJobs<double, double> j{};
+  for (int k = 0; k < nj; ++k) {
+    j.in[k] = in[k];
+    j.w[k] = w[k];
+    j.out[k] = out[k];
+  }
+  conv_f64_exact_dispatch(j, nj, 1, Cin, H, 1, Cin, R, U, pad, 1, E, blocks_for((long long)E * E, 128), s);
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

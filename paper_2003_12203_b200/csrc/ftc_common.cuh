@@ -239,6 +239,10 @@ int launch_kernel_checksums(const float* W, int M, int Ckw, int R, int groups, d
 int launch_conv_f64_exact(const void* in, bool in_f64, const void* w, bool w_f64, double* out,
                           int B, int Cin, int H, int Mo, int Ckw, int R, int U, int pad,
                           int groups, int E, cudaStream_t s);
+// conv_block (conv.hpp:135-145) of up to three (Cd, Cw) pairs at once (Co5 = Cd1*Cw1,
+// Co6 = Cd1*Cw2, Co7 = Cd2*Cw1): one launch, the jobs side by side
+int launch_conv_block3(const double* const in[3], const double* const w[3], double* const out[3], int nj, int Cin,
+                       int H, int R, int U, int pad, int E, cudaStream_t s);
 // bias aggregates: agg[0]=sum_b, agg[1]=sum_mb (BiasAdjuster ctor, checksums.hpp:199-208)
 int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s);
 

@@ -363,15 +363,22 @@ int ensure_cs(EP& e, unsigned want) {
   if (need & FTC_CK_O4)
     CK(launch_conv_f64_exact(L->Dconv, false, L->cw2, true, L->cs[3], d.N, d.C, d.H, 1, d.C, d.R,
                              U, p, 1, E, e.s));
-  if (need & FTC_CK_O5)
-    CK(launch_conv_f64_exact(L->cd1, true, L->cw1, true, L->cs[4], 1, d.C, d.H, 1, d.C, d.R, U, p,
-                             1, E, e.s));
-  if (need & FTC_CK_O6)
-    CK(launch_conv_f64_exact(L->cd1, true, L->cw2, true, L->cs[5], 1, d.C, d.H, 1, d.C, d.R, U, p,
-                             1, E, e.s));
-  if (need & FTC_CK_O7)
-    CK(launch_conv_f64_exact(L->cd2, true, L->cw1, true, L->cs[6], 1, d.C, d.H, 1, d.C, d.R, U, p,
-                             1, E, e.s));
+  {  // Co5 / Co6 / Co7: the conv_blocks of (Cd1, Cw1), (Cd1, Cw2), (Cd2, Cw1) in one launch
+    const double* ins[3];
+    const double* ws[3];
+    double* outs[3];
+    int nj = 0;
+    const double* pin[3] = {L->cd1, L->cd1, L->cd2};
+    const double* pw[3] = {L->cw1, L->cw2, L->cw1};
+    for (int k = 0; k < 3; ++k)
+      if (need & (FTC_CK_O5 << k)) {
+        ins[nj] = pin[k];
+        ws[nj] = pw[k];
+        outs[nj] = L->cs[4 + k];
+        ++nj;
+      }
+    if (nj) CK(launch_conv_block3(ins, ws, outs, nj, d.C, d.H, d.R, U, p, E, e.s));
+  }
   e.cs_have |= need;
   return FTC_OK;
 }
@@ -555,9 +562,12 @@ int detect_and_reload(EP& e, ftc_layer_report* rep, int* resolved) {
     }
     L->ck_exact = true;
   }
-  // Re-establish the CoC-D verdict on exact-order Co5/So5 (bitwise the reference's).
+  // Re-establish the CoC-D verdict on exact-order Co5/So5 (bitwise the reference's).  So6
+  // and So7 come with So5: the three chains run side by side in one launch whose time is
+  // the chain length, and CoC needs them next (values identical whenever computed: O is
+  // unchanged until a scheme patches it)
   CK(ensure_cs(e, FTC_CK_O5));
-  CK(ensure_s(e, FTC_CK_O5));
+  CK(ensure_s(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
   bool clean = false;
   double mrd = 0.0;
   CK(detect_exact_clean(e, &clean, &mrd));
