@@ -270,6 +270,10 @@ __global__ void k_sum_rows(VirtualO v, int N, int M, int E2, uint32_t which, con
 // ~2 ms: the per-lane copy instructions, not the adds, set the pace,
 // tools/ubench_seq.cu.)
 constexpr int kSeqWarps = 3;  // warps per block: the three families of one position
+#ifndef FTC_SEQ_AHEAD
+#define FTC_SEQ_AHEAD 4
+#endif
+constexpr int kSeqAhead = FTC_SEQ_AHEAD;  // 32-term batches loaded ahead of the chain
 template <bool VIRT>
 __global__ void __launch_bounds__(32 * kSeqWarps) k_seq_sums567(VirtualO v, int N, int M, int E2,
                                                                 const int* __restrict__ list,
@@ -306,19 +310,19 @@ __global__ void __launch_bounds__(32 * kSeqWarps) k_seq_sums567(VirtualO v, int 
 #pragma unroll
     for (int u = 0; u < 32; ++u) s = dadd(s, t[u]);
   };
-  double ya = term(0), yb = term(1), yc = term(2);
-  for (long long b = 0; b < nb; b += 3) {
-    const double y0 = ya;
-    ya = term(b + 3);
-    walk(y0);
-    if (b + 1 >= nb) break;
-    const double y1 = yb;
-    yb = term(b + 4);
-    walk(y1);
-    if (b + 2 >= nb) break;
-    const double y2 = yc;
-    yc = term(b + 5);
-    walk(y2);
+  // kSeqAhead batches in flight (registers, rotated by a fully unrolled inner loop)
+  double y[kSeqAhead];
+#pragma unroll
+  for (int k = 0; k < kSeqAhead; ++k) y[k] = term(k);
+  for (long long b = 0; b < nb; b += kSeqAhead) {
+#pragma unroll
+    for (int k = 0; k < kSeqAhead; ++k) {
+      if (b + k < nb) {
+        const double cur = y[k];
+        y[k] = term(b + k + kSeqAhead);
+        walk(cur);
+      }
+    }
   }
   if (lane != 0) return;
   if (agg) {  // BiasAdjuster (checksums.hpp:226-235)

@@ -83,14 +83,16 @@ def vgg19():
     ops, src, i = [], "x", 0
     blocks = [[64, 64], [128, 128], [256] * 4, [512] * 4, [512] * 4]
     for b, widths in enumerate(blocks):
-        for w in widths:
+        for k, w in enumerate(widths):
             i += 1
             ops.append(Conv(src, f"c{i}", w, 3, 1, 1))
-            ops.append(ActPool(f"c{i}", f"a{i}", "relu"))
-            src = f"a{i}"
-        if b < len(blocks) - 1:
-            ops.append(ActPool(src, f"pool{b}", "none", 2, 2))
-            src = f"pool{b}"
+            if k == len(widths) - 1 and b < len(blocks) - 1:
+                # ReLU and the block's 2x2 max-pool in one glue pass: max(relu(x)) == relu(max(x))
+                ops.append(ActPool(f"c{i}", f"pool{b}", "relu", 2, 2))
+                src = f"pool{b}"
+            else:
+                ops.append(ActPool(f"c{i}", f"a{i}", "relu"))
+                src = f"a{i}"
     ops[-1].dst = "out"
     return dict(name="vgg19", batch=64, C=3, H=224, input="normal", ops=ops)
 
@@ -133,14 +135,16 @@ def yolov2():
               [(1024, 3), (512, 1), (1024, 3), (512, 1), (1024, 3)]]
     ops, src, i = [], "x", 0
     for g, layers in enumerate(groups):
-        for (w, r) in layers:
+        for k, (w, r) in enumerate(layers):
             i += 1
             ops.append(Conv(src, f"c{i}", w, r, 1, r // 2))
-            ops.append(ActPool(f"c{i}", f"a{i}", "leaky"))
-            src = f"a{i}"
-        if g < len(groups) - 1:
-            ops.append(ActPool(src, f"pool{g}", "none", 2, 2))
-            src = f"pool{g}"
+            if k == len(layers) - 1 and g < len(groups) - 1:
+                # leaky-ReLU and the group's 2x2 max-pool in one glue pass (monotone act)
+                ops.append(ActPool(f"c{i}", f"pool{g}", "leaky", 2, 2))
+                src = f"pool{g}"
+            else:
+                ops.append(ActPool(f"c{i}", f"a{i}", "leaky"))
+                src = f"a{i}"
     for (w, r, act) in [(1024, 3, "leaky"), (1024, 3, "leaky"), (425, 1, None)]:
         i += 1
         ops.append(Conv(src, f"c{i}", w, r, 1, r // 2))
