@@ -1004,89 +1004,75 @@ struct Co5Scatter {  // optional: the block's share of Co5 = Cd1 (*) Cw1, scatte
 };
 
 // Small-batch staging pass (N <= 32): NHWC copy + exact-order Cd1/Cd2 (+ the Co5
-// scatter) in one read of D.  A block owns 32 channels x 32 positions for every image:
-// all of a 16-image chunk's loads are issued at once (64 per thread in flight), the
-// chunk is transposed through shared memory with ONE barrier pair (t[n][pos][c], stride
-// 33: conflict-free both ways), and each warp stores whole 128-byte channel rows.
+// scatter) in one read of D.  A block owns 8 channels x 32 positions; a thread owns one
+// (channel, position) and has all of a 16-image chunk's loads in flight (its Cd1/Cd2
+// chain is sequential over n, checksums.hpp:100-107), the chunk is transposed through
+// shared memory and stored as 32-byte channel runs of the NHWC rows.  Many small blocks
+// (784 at config 1) keep load and store phases of different blocks overlapped.
 constexpr int kStageImg = 16;
-constexpr size_t kStageSmem = (size_t)kStageImg * 32 * 33 * sizeof(float);
+constexpr int kStageCh = 8;
 __global__ void __launch_bounds__(256) k_nhwc_cd32(const float* __restrict__ D, float* __restrict__ Dt, int C,
                                                   int HW, int nimg, double* __restrict__ cd1,
                                                   double* __restrict__ cd2, Co5Scatter sc) {
-  extern __shared__ float t_dyn[];
-  float(*t)[32][33] = reinterpret_cast<float(*)[32][33]>(t_dyn);
+  __shared__ float t[kStageImg][32][kStageCh + 1];
   constexpr int kScTaps = 9;
-  __shared__ double red[kScTaps][8][32];
+  __shared__ double red[kScTaps][kStageCh][32];
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hw = blockIdx.x * 32 + lane;
   const bool ok = hw < HW;
-  const int c0 = blockIdx.y * 32;
-  double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
+  const int c0 = blockIdx.y * kStageCh, c = c0 + warp;
+  double s1 = 0.0, s2 = 0.0;
   for (int n0 = 0; n0 < nimg; n0 += kStageImg) {
     const int ni = min(kStageImg, nimg - n0);
-    float v[kStageImg][4];
+    float v[kStageImg];
 #pragma unroll
     for (int u = 0; u < kStageImg; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = c0 + warp + 8 * q;
-        v[u][q] = (ok && u < ni) ? __ldg(D + ((long long)(n0 + u) * C + c) * HW + hw) : 0.f;
-      }
+      v[u] = (ok && u < ni) ? __ldg(D + ((long long)(n0 + u) * C + c) * HW + hw) : 0.f;
 #pragma unroll
     for (int u = 0; u < kStageImg; ++u) {
-      if (u >= ni) break;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (cd1) {  // checksums.hpp:100-107: ascending n, FP64, no contraction
-          s1[q] = dadd(s1[q], (double)v[u][q]);
-          s2[q] = dadd(s2[q], dmul((double)(n0 + u), (double)v[u][q]));
-        }
-        t[u][lane][warp + 8 * q] = v[u][q];
+      if (u < ni && cd1) {  // ascending n, FP64, no contraction
+        s1 = dadd(s1, (double)v[u]);
+        s2 = dadd(s2, dmul((double)(n0 + u), (double)v[u]));
       }
+      t[u][lane][warp] = v[u];
     }
     __syncthreads();
-    // 16 images x 32 positions = 512 rows of 32 channels; warp w stores rows w, w+8, ...
-    for (int row = warp; row < ni * 32; row += 8) {
+    // ni images x 32 positions = rows of 8 channels (32 bytes of an NHWC row); a warp
+    // instruction stores 4 rows
+    const int r4 = lane >> 3, ch = lane & 7;
+    for (int row = warp * 4 + r4; row < ni * 32; row += 32) {
       const int u = row >> 5, pl = row & 31, sp = blockIdx.x * 32 + pl;
-      if (sp < HW) Dt[((long long)(n0 + u) * HW + sp) * C + c0 + lane] = t[u][pl][lane];
+      if (sp < HW) Dt[((long long)(n0 + u) * HW + sp) * C + c0 + ch] = t[u][pl][ch];
     }
     __syncthreads();
   }
   pdl_trigger();
   if (cd1 && ok) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long e = (long long)(c0 + warp + 8 * q) * HW + hw;
-      cd1[e] = s1[q];
-      cd2[e] = s2[q];
-    }
+    const long long e = (long long)c * HW + hw;
+    cd1[e] = s1;
+    cd2[e] = s2;
   }
   if (sc.co5) {
-    // Co5 is linear in Cd1: this block's 32 channels x 32 input positions contribute
+    // Co5 is linear in Cd1: this block's 8 channels x 32 input positions contribute
     // sum_c Cd1[c][h][w] * Cw1[c][i][j] to output (x, y) with x*U + i - pad = h (same for
     // y, j); channels are summed through shared memory, one atomic per (position, tap)
     const int RR = sc.R * sc.R;
     const int h = hw / sc.H, w = hw - (hw / sc.H) * sc.H;
     for (int t0 = 0; t0 < RR; t0 += kScTaps) {  // kScTaps taps per round, one barrier each
       const int nt = min(kScTaps, RR - t0);
-      for (int tt = 0; tt < nt; ++tt) {
-        double part = 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) part += s1[q] * sc.cw1[(c0 + warp + 8 * q) * RR + t0 + tt];
-        red[tt][warp][lane] = part;
-      }
+      for (int tt = 0; tt < nt; ++tt) red[tt][warp][lane] = s1 * sc.cw1[c * RR + t0 + tt];
       __syncthreads();
-      for (int tt = warp; tt < nt; tt += 8) {  // warp per tap: channel sum, one atomic per position
+      for (int tt = warp; tt < nt; tt += kStageCh) {  // warp per tap: channel sum, one atomic per position
         if (!ok) continue;
-        double v = 0.0;
+        double a = 0.0;
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) v += red[tt][ww][lane];
+        for (int ww = 0; ww < kStageCh; ++ww) a += red[tt][ww][lane];
         const int tap = t0 + tt, i = tap / sc.R, j = tap - (tap / sc.R) * sc.R;
         const int xs = h + sc.pad - i, ys = w + sc.pad - j;
         if (xs >= 0 && ys >= 0 && xs % sc.U == 0 && ys % sc.U == 0) {
           const int x = xs / sc.U, y = ys / sc.U;
-          if (x < sc.E && y < sc.E) atomicAdd(sc.co5 + x * sc.E + y, v);
+          if (x < sc.E && y < sc.E) atomicAdd(sc.co5 + x * sc.E + y, a);
         }
       }
       __syncthreads();
@@ -1297,16 +1283,10 @@ int launch_nhwc_cd(const float* D, float* Dt, int C, int HW, int n_lo, int nimg,
     return FTC_OK;
   }
   if (n_lo == 0) {
-    const dim3 g((unsigned)((HW + 31) / 32), (unsigned)(C / 32));
+    const dim3 g((unsigned)((HW + 31) / 32), (unsigned)(C / kStageCh));
     Co5Scatter sc{};
     if (co5 && cd1) sc = Co5Scatter{co5->co5, co5->cw1, co5->H, co5->R, co5->U, co5->pad, co5->E};
-    static bool attr[kMaxDevices] = {false};
-    const int dev = current_device();
-    if (!attr[dev]) {
-      FTC_CUDA_CHECK(cudaFuncSetAttribute(k_nhwc_cd32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageSmem));
-      attr[dev] = true;
-    }
-    FTC_LAUNCH_PDL(k_nhwc_cd32, g, dim3(256), kStageSmem, s, D, Dt, C, HW, nimg, cd1, cd2, sc);
+    FTC_LAUNCH_PDL(k_nhwc_cd32, g, dim3(256), 0, s, D, Dt, C, HW, nimg, cd1, cd2, sc);
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }

@@ -187,46 +187,38 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
     }
     return m;
   };
+  // IMG images' windows in flight per thread (8 for k = 1 measured slower: VGG-19 relu
+  // glue 2.55 vs 2.21 ms per step)
+  constexpr int IMG = 2;
   double acc = 0.0;
-  int n = n_lo;
-  for (; n + 2 <= n_hi; n += 2) {  // two images' windows in flight
-    float m0 = -INFINITY, m1 = -INFINITY;
+  for (int n = n_lo; n < n_hi; n += IMG) {
+    const int cnt = min(IMG, n_hi - n);
+    float mv[IMG];
+#pragma unroll
+    for (int u = 0; u < IMG; ++u) mv[u] = (ok && u < cnt) ? pool(src + u * istep) : -INFINITY;
     if (ok) {
-      m0 = pool(src);
-      m1 = pool(src + istep);
-      if (out) {  // out == NULL: staging pass of a caller-supplied D (NHWC + Cd1 only)
-        op[0] = m0;
-        op[ostep] = m1;
+#pragma unroll
+      for (int u = 0; u < IMG; ++u) {
+        if (u < cnt) {
+          if (out) op[u * ostep] = mv[u];  // out == NULL: staging pass of a caller-supplied D
+          acc += (double)mv[u];
+        }
       }
-      acc += (double)m0;
-      acc += (double)m1;
     }
     if (out_t) {
-      tile[0][pl][cl] = m0;
-      tile[1][pl][cl] = m1;
+#pragma unroll
+      for (int u = 0; u < IMG; ++u) tile[u][pl][cl] = mv[u];
       __syncthreads();
       if (spos < plane) {
-        tp[0] = tile[0][wp][wc];
-        tp[(long long)plane * C] = tile[1][wp][wc];
+#pragma unroll
+        for (int u = 0; u < IMG; ++u)
+          if (u < cnt) tp[(long long)u * plane * C] = tile[u][wp][wc];
       }
       __syncthreads();
     }
-    src += 2 * istep;
-    if (op) op += 2 * ostep;
-    if (tp) tp += 2LL * plane * C;
-  }
-  if (n < n_hi) {
-    float m0 = -INFINITY;
-    if (ok) {
-      m0 = pool(src);
-      if (out) op[0] = m0;
-      acc += (double)m0;
-    }
-    if (out_t) {
-      tile[0][pl][cl] = m0;
-      __syncthreads();
-      if (spos < plane) tp[0] = tile[0][wp][wc];
-    }
+    src += IMG * istep;
+    if (op) op += IMG * ostep;
+    if (tp) tp += (long long)IMG * plane * C;
   }
   pdl_trigger();
   const long long per = (long long)C * plane;

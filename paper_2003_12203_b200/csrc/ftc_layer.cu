@@ -826,6 +826,11 @@ int stage_faults(ftc_layer* L, const ftc_fault* faults, int n, cudaStream_t s) {
   return FTC_OK;
 }
 
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 bool has_target(const ftc_fault* f, int n, int t) {
   for (int q = 0; q < n; ++q)
     if (f[q].target == t) return true;
@@ -1140,20 +1145,30 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     // the detect kernels re-zero: on a failed launch clear them here, or every later
     // call on this layer would read stale partial sums as a CoC-D mismatch
     int st = timed_conv(L, D, L->Wcur, O, L->n_out_faults > 0, false, s, &fd, dt_ready);
+    // CoC-D on the layer's side stream (forked after the conv, so the caller's next
+    // kernels do not wait for the compare) is an experiment, FTC_DETECT_SIDE=1: it saved
+    // ~0.8% on VGG-19 and cost config 1 ~4 us of fork/join, so the compare stays in line
+    cudaStream_t ds = s;
+    static const bool detect_side = getenv_flag("FTC_DETECT_SIDE");
+    if (st == FTC_OK && detect_side) {
+      if (cudaEventRecord(L->ev_start, s) == cudaSuccess && cudaStreamWaitEvent(L->side, L->ev_start, 0) == cudaSuccess)
+        ds = L->side;
+    }
     if (st == FTC_OK) {
       if (co5_in || co5_ready)
         st = launch_detect_fused(L->co5f, L->so5acc, d.N, L->E2, d.bias_enabled ? 1 : 0, L->agg, plan->tau,
-                                 L->fstats, L->fticket, L->fstats_hd, s);
+                                 L->fstats, L->fticket, L->fstats_hd, ds);
       else
         st = launch_co5_detect(cd1_use, L->cw1, L->co5f, L->so5acc, d.N, d.C, d.H, d.R, d.stride, d.pad, L->E,
-                               d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats, L->fticket, L->fstats_hd, s);
+                               d.bias_enabled ? 1 : 0, L->agg, plan->tau, L->fstats, L->fticket, L->fstats_hd, ds);
     }
     if (st != FTC_OK) {
+      cudaStreamSynchronize(ds);
       cudaMemsetAsync(L->co5f, 0, L->E2 * sizeof(double), s);
       cudaMemsetAsync(L->so5acc, 0, L->E2 * sizeof(double), s);
       return st;
     }
-    FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, s));
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_done, ds));
     L->inflight = true;
     return FTC_OK;
   }
@@ -1285,8 +1300,9 @@ int ftc_protected_conv(ftc_layer* L, const ftc_plan* plan, const float* D, float
 int ftc_layer_detect_record(ftc_layer* L, void* dst, void* stream) {
   if (!L || !dst) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
   if (!L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "no protected call in flight");
-  // stream-ordered after the detect kernel, which published {flagged, max_rel_dev} into
-  // the mapped record (device alias) before its grid completed
+  // stream-ordered after the detect kernel (side stream: ev_done), which published
+  // {flagged, max_rel_dev} into the mapped record (device alias) before its grid completed
+  FTC_CUDA_CHECK(cudaStreamWaitEvent((cudaStream_t)stream, L->ev_done, 0));
   FTC_CUDA_CHECK(cudaMemcpyAsync(dst, L->fstats_hd, sizeof(DetectStats), cudaMemcpyDeviceToDevice,
                                  (cudaStream_t)stream));
   return FTC_OK;

@@ -7,7 +7,12 @@ import sys
 
 
 def rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep, or the `ncu -i rep --page raw --csv` export of one (profiles keep
+    the export; the reports themselves exceed what a GPU call can bring back)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     lines = [l for l in out.splitlines() if l.startswith('"')]
     r = list(csv.reader(io.StringIO("\n".join(lines))))
     hdr, units, data = r[0], r[1], r[2:]

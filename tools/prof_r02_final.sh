@@ -13,11 +13,19 @@ for w in vgg19 config1 alexnet resnet18 yolov2; do
   timeout 900 ncu --nvtx --nvtx-include "timed_step/" $M --log-file gpurun_out/${PFX}_launches_$w.csv python bench.py --workload $w $B > gpurun_out/${PFX}_ncu_$w.log 2>&1
 done
 F="--set full --clock-control none --import-source on --nvtx --nvtx-include timed_step/"
-timeout 1500 ncu $F -k regex:k_conv_tc -c 16 -o gpurun_out/${PFX}_vgg_convs python bench.py --workload vgg19 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_vgg.log 2>&1
-timeout 1500 ncu $F -k regex:k_conv_tc -c 20 -o gpurun_out/${PFX}_resnet_convs python bench.py --workload resnet18 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_resnet.log 2>&1
-timeout 1500 ncu $F -k regex:k_conv_tc -c 21 -o gpurun_out/${PFX}_yolo_convs python bench.py --workload yolov2 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_yolo.log 2>&1
-timeout 900 ncu $F -k regex:"k_act_pool|k_cd1|k_nhwc|k_detect|k_co5" -c 12 -o gpurun_out/${PFX}_vgg_glue python bench.py --workload vgg19 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_glue.log 2>&1
-timeout 900 ncu $F -c 3 -o gpurun_out/${PFX}_config1 python bench.py --workload config1 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_c1.log 2>&1
+# --set full reports are exported to CSV (raw page) and deleted: a GPU call brings back
+# at most 64 MiB of gpurun_out/; the config-1 report (3 kernels) is kept whole
+R=/tmp/ncurep; mkdir -p $R
+full() {  # name, kernel regex, count, workload
+  timeout 1500 ncu $F -k regex:"$2" -c $3 -o $R/$1 python bench.py --workload $4 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_$1.log 2>&1
+  ncu -i $R/$1.ncu-rep --page raw --csv > gpurun_out/${PFX}_$1_raw.csv 2>/dev/null
+}
+full vgg_convs k_conv_tc 16 vgg19
+full resnet_convs k_conv_tc 20 resnet18
+full yolo_convs k_conv_tc 21 yolov2
+full vgg_glue "k_act_pool|k_cd1|k_nhwc|k_detect|k_co5" 12 vgg19
+full config1 "k_" 3 config1
+cp $R/config1.ncu-rep gpurun_out/${PFX}_config1.ncu-rep
 FAULT_REPS=5 timeout 600 python tools/fault_one.py > gpurun_out/${PFX}_fault.log 2>&1
 timeout 900 ncu $M --log-file gpurun_out/${PFX}_fault_launches.csv env FAULT_REPS=1 python tools/fault_one.py > gpurun_out/${PFX}_fault_ncu.log 2>&1
 echo done
