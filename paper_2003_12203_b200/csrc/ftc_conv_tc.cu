@@ -102,6 +102,17 @@ template <int BN>
 constexpr int group_chunks() {
   return BN >= 96 ? 1 : FTC_GROUP_NARROW;
 }
+// one tcgen05.commit per accumulator group (a ring of 8 "group done" barriers that the
+// producers, the B loader and the epilogue all wait on) instead of four per chunk --
+// same speed (the commits were not the limiter), fewer instructions on the issuers
+#ifndef FTC_ONE_COMMIT
+#define FTC_ONE_COMMIT 1
+#endif
+constexpr bool kOneCommit = FTC_ONE_COMMIT;
+#ifndef FTC_SPLIT_LOADER
+#define FTC_SPLIT_LOADER 0
+#endif
+constexpr bool kSplitLoader = FTC_SPLIT_LOADER;
 #ifndef FTC_KAS
 #define FTC_KAS 4
 #endif
@@ -231,6 +242,16 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// wait until accumulator group j of this CTA has completed (kOneCommit ring of 8)
+__device__ __forceinline__ void gdone_wait(uint32_t gdone0, uint32_t j, bool lazy) {
+  const uint32_t bar = gdone0 + 8 * (j & 7u), ph = (j >> 3) & 1u;
+  if (lazy) {
+    while (!mbar_try_wait(bar, ph)) __nanosleep(64);
+  } else {
+    while (!mbar_try_wait(bar, ph)) {
+    }
+  }
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -331,8 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
   const uint32_t fullA0 = bar_base, emptyA0 = bar_base + 8 * 8;
   const uint32_t fullB0 = bar_base + 8 * 16, emptyB0 = fullB0 + 8 * kMaxSB;
   const uint32_t accf0 = emptyB0 + 8 * kMaxSB, acce0 = accf0 + 8 * 4;
-  const uint32_t fullAs0 = acce0 + 8 * 4, emptyAs0 = fullAs0 + 8 * kAS;  // MODE 2 A ring
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kMaxSB + 8 + 2 * kAS);
+  const uint32_t gdone0 = acce0 + 8 * 4;  // kOneCommit: group j done = gdone[j % 8]
+  const uint32_t fullAs0 = gdone0 + 8 * 8, emptyAs0 = fullAs0 + 8 * kAS;  // MODE 2 A ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kMaxSB + 8 + 8 + 2 * kAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (!TMAA)
@@ -346,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       mbar_init(fullB0 + 8 * s, 1);
       mbar_init(emptyB0 + 8 * s, 1);
     }
+    for (int b = 0; b < 8; ++b) mbar_init(gdone0 + 8 * b, 1);
     for (int b = 0; b < kNX; ++b) {
       mbar_init(accf0 + 8 * b, 1);
       mbar_init(acce0 + 8 * b, kEpiThreads / 32);
@@ -391,9 +414,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       // split hi/lo and store them to the TMEM half-stage like the gather paths
       uint32_t sa = 0, pha = 0;
       const bool pprof2 = (a.dbg & 64) && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kProdWarps - 1);
-      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+      const uint32_t ngt = (uint32_t)(a.nkc + kG - 1) / (uint32_t)kG;
+      uint32_t jh[4] = {0, 0, 0, 0}, tlp = 0;  // groups of the last 4 chunks (kOneCommit)
+      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tlp) {
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
           const uint32_t s = hs, ph = hph;
+          const uint32_t jprev = jh[kSA - 1];  // group of this slot's previous chunk
+          jh[3] = jh[2];
+          jh[2] = jh[1];
+          jh[1] = jh[0];
+          jh[0] = tlp * ngt + (uint32_t)kc / (uint32_t)kG;
           hs += 2;
           if (hs >= (uint32_t)kHS) { hs -= (uint32_t)kHS; hph ^= 1u; }
           const uint32_t sa_c = sa, pha_c = pha;
@@ -420,7 +450,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
             const float l = __uint_as_float(v[e]) - __uint_as_float(h);
             lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
           }
-          mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+          if (!kOneCommit) mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+          else if (g >= (uint32_t)kSA) gdone_wait(gdone0, jprev, false);
           if (warp == 0) TC_TRACE(pprof2, 1, g);
           tc_after();
           const uint32_t col = tmem + lane_off + a_col0 + s * 32u;
@@ -492,9 +523,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       setup(blockIdx.x);
       gather(0, vn);
     }
-    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+    const uint32_t ngt0 = (uint32_t)(a.nkc + kG - 1) / (uint32_t)kG;
+    uint32_t jh0[4] = {0, 0, 0, 0}, tlp0 = 0;  // groups of the last 4 chunks (kOneCommit)
+    for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tlp0) {
       for (int kc = 0; kc < a.nkc; ++kc, ++g) {
         const uint32_t s = hs, ph = hph;
+        const uint32_t jprev = jh0[kSA - 1];
+        jh0[3] = jh0[2];
+        jh0[2] = jh0[1];
+        jh0[1] = jh0[0];
+        jh0[0] = tlp0 * ngt0 + (uint32_t)kc / (uint32_t)kG;
         hs += 2;
         if (hs >= (uint32_t)kHS) { hs -= (uint32_t)kHS; hph ^= 1u; }
         float v[16];
@@ -519,7 +557,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
         }
         if (warp == 0) TC_TRACE(pprof, 0, g);
-        mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+        if (!kOneCommit) mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
+        else if (g >= (uint32_t)kSA) gdone_wait(gdone0, jprev, false);
         if (warp == 0) TC_TRACE(pprof, 1, g);
         tc_after();
         if (!(a.dbg & 2)) {
@@ -536,11 +575,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
     }
     }
   } else if (warp == kLoaderWarp) {
-    // ================= B loader =================
-    if (lane == 0) {
+    // ================= loader =================
+    // lane 0 streams the A (TMA im2col) and B stages.  FTC_SPLIT_LOADER=1 moves the A
+    // stream to lane 1 (independent thread scheduling); measured 12-20% slower on the
+    // BN = 128 layers, so off
+    const bool doB = lane == 0;
+    const bool doA = TMAA && (kSplitLoader ? lane == 1 : lane == 0);
+    if (doA || doB) {
       uint32_t g = 0, sB = 0, phB = 0, sa = 0, pha = 0;
       const int ncb = (GROUPED ? a.Ckw : a.C) / 32;
-      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+      const uint32_t ngtl = (uint32_t)(a.nkc + kG - 1) / (uint32_t)kG;
+      uint32_t jb[4] = {0, 0, 0, 0}, tll = 0;  // groups of the last 4 chunks (kOneCommit)
+      for (int t = blockIdx.x; t < ntile_total; t += gridDim.x, ++tll) {
         const int nt = t / a.npt;
         const int cg = GROUPED ? nt / a.ntg * a.Ckw : 0;  // the tile's group's first channel
         const float* src = a.Wp + (long long)nt * a.nkc * 2 * BN * kBK;
@@ -548,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         const long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
         const int n0 = (int)(p0 / E2), f0 = (int)(p0 % E2);
         const int cw = (f0 % E) * a.U - a.pad, ch = (f0 / E) * a.U - a.pad;
-        if constexpr (MODE == 0) {
+        if (MODE == 0 && doB) {
           // register-gather layers: L2-prefetch the input rows this CTA's NEXT tile gathers
           // (its window rows of every channel, one bulk prefetch per channel) a tile ahead,
           // so its compulsory misses hit L2 instead of DRAM
@@ -574,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         }
         int ti = 0, tj = 0, cb = 0;  // K chunk kc = ((ti*R + tj)*ncb + cb)
         for (int kc = 0; kc < a.nkc; ++kc, ++g) {
-          if constexpr (TMAA) {
+          if (doA) {
             mbar_wait_lazy(emptyAs0 + 8 * sa, pha ^ 1u);
             TC_TRACE((a.dbg & 64) && blockIdx.x == 0, 12, g);
             if (a.dbg & 1) {  // profiling: skip the A gather
@@ -590,9 +636,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
               if (++tj == R) { tj = 0; ++ti; }
             }
           }
+          if (!doB) continue;
           const uint32_t s = sB, ph = phB;
           if (++sB == (uint32_t)SB) { sB = 0; phB ^= 1u; }
-          mbar_wait_lazy(emptyB0 + 8 * s, ph ^ 1u);
+          const uint32_t jprev = SB == 2 ? jb[1] : SB == 3 ? jb[2] : jb[3];  // this stage's previous chunk
+          jb[3] = jb[2];
+          jb[2] = jb[1];
+          jb[1] = jb[0];
+          jb[0] = tll * ngtl + (uint32_t)kc / (uint32_t)kG;
+          if (!kOneCommit) mbar_wait_lazy(emptyB0 + 8 * s, ph ^ 1u);
+          else if (g >= (uint32_t)SB) gdone_wait(gdone0, jprev, true);
           TC_TRACE((a.dbg & 64) && blockIdx.x == 0, 8, g);
           if (a.dbg & 16) {
             mbar_arrive(fullB0 + 8 * s);
@@ -684,14 +737,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
               }
           }
           TC_TRACE(mprof, 5, c0);
+          if (kOneCommit) {
+            mma_commit(gdone0 + 8 * (j & 7u));  // frees the group's A slots, B stages, accumulator
+          } else {
 #pragma unroll
-          for (int u = 0; u < kG; ++u)
-            if ((uint32_t)u < nc) {
-              mma_commit(emptyA0 + 8 * (2u * cs[u]));
-              mma_commit(emptyA0 + 8 * (2u * cs[u] + 1u));
-              mma_commit(emptyB0 + 8 * bs[u]);
-            }
-          mma_commit(accf0 + 8 * xbuf);
+            for (int u = 0; u < kG; ++u)
+              if ((uint32_t)u < nc) {
+                mma_commit(emptyA0 + 8 * (2u * cs[u]));
+                mma_commit(emptyA0 + 8 * (2u * cs[u] + 1u));
+                mma_commit(emptyB0 + 8 * bs[u]);
+              }
+            mma_commit(accf0 + 8 * xbuf);
+          }
         }
         __syncwarp();
       }
@@ -779,7 +836,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       for (int kc = 0; kc < ngt; ++kc, ++gq) {
         const uint32_t b = gq % (uint32_t)kNX;
         xb = tmem + lane_off + b * (uint32_t)BN + (uint32_t)(half * HALF);
-        mbar_wait_lazy(accf0 + 8 * b, (gq / (uint32_t)kNX) & 1u);
+        if (kOneCommit)
+          gdone_wait(gdone0, gq, true);
+        else
+          mbar_wait_lazy(accf0 + 8 * b, (gq / (uint32_t)kNX) & 1u);
         TC_TRACE(eprof, 6, tl * (uint32_t)a.nkc + (uint32_t)(kc * kG));
         tc_after();
 #pragma unroll
