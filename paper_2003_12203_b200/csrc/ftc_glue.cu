@@ -130,6 +130,136 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
   }
 }
 
+// k = 1 (activation only) producer of a protected conv's input, positions % 4 == 0:
+// act(O) -> D (NCHW, float4 stores) + the TMA engine's NHWC copy + the clean-path Cd1
+// slabs, 32 channels x 32 positions per block.  A thread owns one channel x 4 positions
+// (one 16-byte load per image) and keeps four images' loads in flight (~128 KB per SM
+// at full occupancy: the 8-position variant held 16 KB and sat on memory latency at
+// ~3.2 TB/s, r02b ncu); the NHWC rows go out through a shared-memory transpose, one
+// barrier pair per four images.
+// POOL2: 2x2 stride-2 max-pool after the activation (Ho % 4 == 0, so a thread's 4
+// output positions share a row and read two rows of 8 inputs: four 16-byte loads).
+constexpr int kV4Img = 4;
+template <int ACT, bool POOL2>
+__global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in, float* __restrict__ out,
+                                                   float* __restrict__ out_t, int N, int NG, int C, int HW,
+                                                   double* __restrict__ ws, long long tick_off, long long slab_off,
+                                                   int Ho) {
+  __shared__ float tile[kV4Img][32][33];  // [image][position][channel]
+  const int tid = threadIdx.x;
+  const int cl = tid >> 3, p4 = (tid & 7) * 4;  // load role: channel row, 4 positions
+  const int c = blockIdx.y * 32 + cl, pos = blockIdx.x * 32 + p4;
+  const int wc = tid & 31, wp = tid >> 5;     // store role: lane = channel, warp = position row
+  const int g = blockIdx.z, G = gridDim.z;
+  const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
+  const bool ok = pos < HW;  // HW % 4 == 0: the whole float4 is in range
+  const long long plane_c = (long long)C * HW;
+  // input: HW positions per plane without pooling, (2 Ho)^2 with it
+  const int Hi = POOL2 ? 2 * Ho : 0;
+  const long long iplane = POOL2 ? (long long)Hi * Hi : HW;
+  const long long istep4 = (long long)C * iplane / 4;
+  long long ioff = pos;  // element offset of this thread's first input in its plane
+  if (POOL2) {
+    const int ox = pos / Ho, oy = pos - (pos / Ho) * Ho;
+    ioff = (long long)(2 * ox) * Hi + 2 * oy;
+  }
+  pdl_wait();
+  const float4* src = reinterpret_cast<const float4*>(in + ((long long)n_lo * C + c) * iplane + ioff);
+  float4* op = out ? reinterpret_cast<float4*>(out + ((long long)n_lo * C + c) * HW + pos) : nullptr;
+  const long long step4 = plane_c / 4;
+  const int row4 = POOL2 ? Hi / 4 : 0;  // one input row in float4s
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int n = n_lo; n < n_hi; n += kV4Img) {
+    const int cnt = min(kV4Img, n_hi - n);
+    float4 v[kV4Img];
+    if (POOL2) {
+      float4 r[kV4Img][4];
+#pragma unroll
+      for (int u = 0; u < kV4Img; ++u)
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4)
+          r[u][k4] = (ok && u < cnt) ? __ldcs(src + u * istep4 + (k4 >> 1) * row4 + (k4 & 1))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kV4Img; ++u) {
+        // output j of the 4 takes input columns 2j, 2j+1 of both rows (max of act, the
+        // pooling kernels' -inf start)
+        const float a0[8] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w, r[u][1].x, r[u][1].y, r[u][1].z, r[u][1].w};
+        const float a1[8] = {r[u][2].x, r[u][2].y, r[u][2].z, r[u][2].w, r[u][3].x, r[u][3].y, r[u][3].z, r[u][3].w};
+        float m[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float mm = -INFINITY;
+          mm = fmaxf(mm, act_fn(a0[2 * j], ACT));
+          mm = fmaxf(mm, act_fn(a0[2 * j + 1], ACT));
+          mm = fmaxf(mm, act_fn(a1[2 * j], ACT));
+          mm = fmaxf(mm, act_fn(a1[2 * j + 1], ACT));
+          m[j] = mm;
+        }
+        v[u] = make_float4(m[0], m[1], m[2], m[3]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kV4Img; ++u)
+        v[u] = (ok && u < cnt) ? __ldcs(src + u * istep4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kV4Img; ++u) {
+        v[u].x = act_fn(v[u].x, ACT);
+        v[u].y = act_fn(v[u].y, ACT);
+        v[u].z = act_fn(v[u].z, ACT);
+        v[u].w = act_fn(v[u].w, ACT);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV4Img; ++u) {
+      if (ok && u < cnt) {
+        if (op) op[u * step4] = v[u];
+        acc[0] += (double)v[u].x;
+        acc[1] += (double)v[u].y;
+        acc[2] += (double)v[u].z;
+        acc[3] += (double)v[u].w;
+      }
+    }
+    if (out_t) {
+#pragma unroll
+      for (int u = 0; u < kV4Img; ++u) {
+        tile[u][p4 + 0][cl] = v[u].x;
+        tile[u][p4 + 1][cl] = v[u].y;
+        tile[u][p4 + 2][cl] = v[u].z;
+        tile[u][p4 + 3][cl] = v[u].w;
+      }
+      __syncthreads();
+      // kV4Img images x 32 positions of 32-channel NHWC rows; warp wp stores rows wp, wp+8, ...
+      for (int row = wp; row < cnt * 32; row += 8) {
+        const int u = row >> 5, pl = row & 31, sp = blockIdx.x * 32 + pl;
+        if (sp < HW) out_t[((long long)(n + u) * HW + sp) * C + blockIdx.y * 32 + wc] = tile[u][pl][wc];
+      }
+      __syncthreads();
+    }
+    src += kV4Img * istep4;
+    if (op) op += kV4Img * step4;
+  }
+  pdl_trigger();
+  const long long per = plane_c;
+  const long long e = (long long)c * HW + pos;
+  if (ok) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ws[slab_off + per * g + e + q] = acc[q];
+  }
+  const int tl = blockIdx.y * gridDim.x + blockIdx.x;
+  if (ws_arrive(ws, tick_off, tl, G)) {
+    if (ok) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double t = 0.0;
+        for (int gg = 0; gg < G; ++gg) t += __ldcg(ws + slab_off + per * gg + e + q);
+        ws[e + q] = t;
+      }
+    }
+    if (tid == 0) ws_tickets(ws, tick_off)[tl] = 0u;
+  }
+}
+
 // k_act_pool_t over a group of images per block, also summing each thread's (c, position)
 // over the group in FP64 into the Cd1 workspace (the consumer conv's clean-path Cd1)
 template <int KT, int ACT>
@@ -441,6 +571,31 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
   const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
   const int G = act_pool_groups(N, C, Ho);
   const int NG = (N + G - 1) / G;
+  static const bool v4_off = getenv("FTC_GLUE_V4") && atoi(getenv("FTC_GLUE_V4")) == 0;
+  const bool plain = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0;
+  const bool pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0;
+  if ((plain || pool2) && C % 32 == 0 && !v4_off && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+      (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    // 32-position tiles: fewer tiles than the 8-position layout the workspace is sized
+    // for, and no more image groups than it holds
+    const int HW = Ho * Ho;
+    const dim3 gv((unsigned)((HW + 31) / 32), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
+#define FTC_V4(A, P)                                                                                              \
+  FTC_LAUNCH_PDL((k_act_v4_cd1<A, P>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws, w.tick_off, w.slab_off, \
+                 Ho)
+    if (pool2) {
+      if (act == 1) FTC_V4(1, true);
+      else if (act == 2) FTC_V4(2, true);
+      else FTC_V4(0, true);
+    } else {
+      if (act == 1) FTC_V4(1, false);
+      else if (act == 2) FTC_V4(2, false);
+      else FTC_V4(0, false);
+    }
+#undef FTC_V4
+    FTC_CUDA_CHECK(cudaGetLastError());
+    return FTC_OK;
+  }
   const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
 #define FTC_APT2(KT, ACT) \
   FTC_LAUNCH_PDL(k_act_pool_t_cd1<KT, ACT>, g, dim3(256), 0, st, in, out, out_t, N, NG, C, H, k, s, p, Ho, ws, \
