@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
 // POOL2: 2x2 stride-2 max-pool after the activation (Ho % 4 == 0, so a thread's 4
 // output positions share a row and read two rows of 8 inputs: four 16-byte loads).
 constexpr int kV4Img = 4;
-template <int ACT, bool POOL2>
+template <int ACT, bool POOL2, bool VEC = true>
 __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in, float* __restrict__ out,
                                                    float* __restrict__ out_t, int N, int NG, int C, int HW,
                                                    double* __restrict__ ws, long long tick_off, long long slab_off,
@@ -152,7 +152,11 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
   const int wc = tid & 31, wp = tid >> 5;     // store role: lane = channel, warp = position row
   const int g = blockIdx.z, G = gridDim.z;
   const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
-  const bool ok = pos < HW;  // HW % 4 == 0: the whole float4 is in range
+  // VEC: HW % 4 == 0 and 16-byte aligned tensors, so a thread's 4 positions are one
+  // float4; otherwise four scalar accesses with per-element bounds (odd extents such as
+  // the 57x57 / 55x55 pad and crop outputs of ResNet-18's stride-2 blocks)
+  const bool ok = pos < HW;
+  const int nq = VEC ? 4 : min(4, HW - pos);
   const long long plane_c = (long long)C * HW;
   // input: HW positions per plane without pooling, (2 Ho)^2 with it
   const int Hi = POOL2 ? 2 * Ho : 0;
@@ -164,9 +168,10 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
     ioff = (long long)(2 * ox) * Hi + 2 * oy;
   }
   pdl_wait();
+  // (with !VEC the pointers are only carriers of the element address: accessed as float)
   const float4* src = reinterpret_cast<const float4*>(in + ((long long)n_lo * C + c) * iplane + ioff);
   float4* op = out ? reinterpret_cast<float4*>(out + ((long long)n_lo * C + c) * HW + pos) : nullptr;
-  const long long step4 = plane_c / 4;
+  const long long step4 = plane_c / 4;  // VEC only
   const int row4 = POOL2 ? Hi / 4 : 0;  // one input row in float4s
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int n = n_lo; n < n_hi; n += kV4Img) {
@@ -199,9 +204,21 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
         v[u] = make_float4(m[0], m[1], m[2], m[3]);
       }
     } else {
+      if (VEC) {
 #pragma unroll
-      for (int u = 0; u < kV4Img; ++u)
-        v[u] = (ok && u < cnt) ? __ldcs(src + u * istep4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < kV4Img; ++u)
+          v[u] = (ok && u < cnt) ? __ldcs(src + u * istep4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const float* sf = in + ((long long)n * C + c) * iplane + ioff;  // element addressing
+#pragma unroll
+        for (int u = 0; u < kV4Img; ++u) {
+          float e4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            e4[q] = (ok && u < cnt && q < nq) ? __ldcs(sf + (long long)u * C * iplane + q) : 0.f;
+          v[u] = make_float4(e4[0], e4[1], e4[2], e4[3]);
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kV4Img; ++u) {
         v[u].x = act_fn(v[u].x, ACT);
@@ -213,11 +230,22 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
 #pragma unroll
     for (int u = 0; u < kV4Img; ++u) {
       if (ok && u < cnt) {
-        if (op) op[u * step4] = v[u];
-        acc[0] += (double)v[u].x;
-        acc[1] += (double)v[u].y;
-        acc[2] += (double)v[u].z;
-        acc[3] += (double)v[u].w;
+        if (VEC) {
+          if (op) op[u * step4] = v[u];
+          acc[0] += (double)v[u].x;
+          acc[1] += (double)v[u].y;
+          acc[2] += (double)v[u].z;
+          acc[3] += (double)v[u].w;
+        } else {
+          const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          float* of = out ? out + ((long long)(n + u) * C + c) * HW + pos : nullptr;  // element addressing
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nq) {
+              if (of) of[q] = e4[q];
+              acc[q] += (double)e4[q];
+            }
+        }
       }
     }
     if (out_t) {
@@ -244,13 +272,15 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
   const long long e = (long long)c * HW + pos;
   if (ok) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ws[slab_off + per * g + e + q] = acc[q];
+    for (int q = 0; q < 4; ++q)
+      if (q < nq) ws[slab_off + per * g + e + q] = acc[q];
   }
   const int tl = blockIdx.y * gridDim.x + blockIdx.x;
   if (ws_arrive(ws, tick_off, tl, G)) {
     if (ok) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
+        if (q >= nq) continue;
         double t = 0.0;
         for (int gg = 0; gg < G; ++gg) t += __ldcg(ws + slab_off + per * gg + e + q);
         ws[e + q] = t;
@@ -474,8 +504,16 @@ __global__ void __launch_bounds__(256) k_pad_crop(const float* __restrict__ in, 
   if (idx >= Ho * Ho) return;
   const int x = idx / Ho - lo, y = idx - (idx / Ho) * Ho - lo;
   const bool ok = x >= 0 && x < H && y >= 0 && y < H;
-  for (int nc = blockIdx.y; nc < NC; nc += gridDim.y)
-    out[(long long)nc * Ho * Ho + idx] = ok ? __ldg(in + ((long long)nc * H + x) * H + y) : 0.f;
+  // four planes per step: four loads in flight per thread (one left the pass at 1.7 TB/s)
+  for (int nc0 = blockIdx.y * 4; nc0 < NC; nc0 += gridDim.y * 4) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = (ok && nc0 + u < NC) ? __ldg(in + ((long long)(nc0 + u) * H + x) * H + y) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (nc0 + u < NC) out[(long long)(nc0 + u) * Ho * Ho + idx] = v[u];
+  }
 }
 
 inline int grid_for(long long n) {
@@ -572,10 +610,12 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
   const int G = act_pool_groups(N, C, Ho);
   const int NG = (N + G - 1) / G;
   static const bool v4_off = getenv("FTC_GLUE_V4") && atoi(getenv("FTC_GLUE_V4")) == 0;
-  const bool plain = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0;
-  const bool pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0;
-  if ((plain || pool2) && C % 32 == 0 && !v4_off && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
-      (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  // the scalar-access form only pays on large planes (AlexNet's 13x13: 80 vs 75 us)
+  const bool vec = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0 && aligned;
+  const bool plain = vec || (k == 1 && s == 1 && p == 0 && H * H >= 1024);
+  const bool pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0 && aligned;
+  if ((plain || pool2) && C % 32 == 0 && !v4_off) {
     // 32-position tiles: fewer tiles than the 8-position layout the workspace is sized
     // for, and no more image groups than it holds
     const int HW = Ho * Ho;
@@ -587,10 +627,18 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
       if (act == 1) FTC_V4(1, true);
       else if (act == 2) FTC_V4(2, true);
       else FTC_V4(0, true);
-    } else {
+    } else if (vec) {
       if (act == 1) FTC_V4(1, false);
       else if (act == 2) FTC_V4(2, false);
       else FTC_V4(0, false);
+    } else {
+#define FTC_V1(A)                                                                                                  \
+  FTC_LAUNCH_PDL((k_act_v4_cd1<A, false, false>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws, w.tick_off, \
+                 w.slab_off, Ho)
+      if (act == 1) FTC_V1(1);
+      else if (act == 2) FTC_V1(2);
+      else FTC_V1(0);
+#undef FTC_V1
     }
 #undef FTC_V4
     FTC_CUDA_CHECK(cudaGetLastError());
@@ -709,7 +757,8 @@ int ftc_glue_pad_crop(const float* in, float* out, int32_t N, int32_t C, int32_t
     set_error(FTC_CONFIG_ERROR, "bad pad/crop");
     return FTC_CONFIG_ERROR;
   }
-  const dim3 g((unsigned)((Ho * Ho + 255) / 256), (unsigned)(N * C < 65535 ? N * C : 65535));
+  const int ny = (N * C + 3) / 4;
+  const dim3 g((unsigned)((Ho * Ho + 255) / 256), (unsigned)(ny < 65535 ? ny : 65535));
   FTC_LAUNCH(k_pad_crop<<<g, 256, 0, (cudaStream_t)stream>>>(in, out, N * C, H, lo, Ho));
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
