@@ -40,7 +40,7 @@
 // magnitude |O|*sqrt(64/K); within a group the 16 small correction products go in first
 // (while the partial is small: they lose nothing) and the 8 main products last, so a
 // group costs 8 truncations of the partial, independent of K.  The partials are summed in registers
-// (FP64 for BN <= 64, FP32 for wider tiles, where 64 doubles per thread would not fit).
+// (FP32).
 // TMEM: [0, BN) X_0, [BN, 2*BN) X_1, then up to 8 A half-stages of 32 columns
 // (16 hi + 16 lo).
 #include <cuda.h>
@@ -109,6 +109,11 @@ constexpr int group_chunks() {
 #define FTC_ONE_COMMIT 1
 #endif
 constexpr bool kOneCommit = FTC_ONE_COMMIT;
+// epilogue running sums of the group partials in FP32 for every tile width (FP64 for
+// BN <= 64 put the narrow layers' drain on the issuers' critical path: VGG c2 traces)
+#ifndef FTC_EPI_F32
+#define FTC_EPI_F32 1
+#endif
 #ifndef FTC_SPLIT_LOADER
 #define FTC_SPLIT_LOADER 0
 #endif
@@ -813,10 +818,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       const int n = valid ? (int)(p / E2) : 0;
       const int f = valid ? (int)(p % E2) : 0;
       const int x = f / E, y = f - (f / E) * E;
-      // running sums of the group partials, in group order: FP64 while the per-thread
-      // values fit the register budget (BN <= 64), FP32 beyond (still several times
-      // closer to the exact conv than the reference's sequential FP32 loop)
-      using acc_t = typename std::conditional<(HALF <= 32), double, float>::type;
+      // running sums of the group partials, in group order, in FP32 (several times closer
+      // to the exact conv than the reference's sequential FP32 loop; FP64 sums for the
+      // BN <= 64 tiles made the drain the issuers' bottleneck: VGG c2 2602 -> 2156 us)
+      using acc_t = typename std::conditional<(HALF <= 32 && !FTC_EPI_F32), double, float>::type;
       acc_t sum[HALF];
 #pragma unroll
       for (int jj = 0; jj < HALF; ++jj) sum[jj] = acc_t(0);
