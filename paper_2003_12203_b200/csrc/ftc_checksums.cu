@@ -532,6 +532,64 @@ __global__ void k_co5_taps(const double* __restrict__ cw1, int C, int H, int R, 
 // bias not yet removed), Co5 by its checksum warp.  One thread per position compares
 // them (values_differ, checksums.hpp:54-60) and re-zeroes So5; the last block publishes
 // {flagged, max_rel_dev} into the mapped host record and re-arms the counters.
+// One-block CoC-D for E2 <= kDetect1Max (experiment, FTC_DETECT_1BLOCK=1): a thread
+// walks E2 / 1024 positions, the block reduces the count and the max deviation through
+// shared memory and thread 0 publishes the record -- no grid-wide fence/ticket/atomics.
+// Same 8 us under ncu as the multi-block kernel, and config 1's protected step went from
+// 69 to 86 us with it (one SM, behind the persistent conv), so it is off.
+constexpr int kDetect1Max = 8192;
+__global__ void __launch_bounds__(1024) k_detect_fused1(double* __restrict__ co5, double* __restrict__ so5, int N,
+                                                       int E2, int bias, const double* agg, double tau,
+                                                       DetectStats* host_out) {
+  __shared__ int s_bad[32];
+  __shared__ unsigned long long s_dev[32];
+  pdl_trigger();
+  pdl_wait();
+  int bad = 0;
+  unsigned long long devb = 0ull;
+  const double bsum = bias ? (double)N * agg[0] : 0.0;
+  for (int f = threadIdx.x; f < E2; f += blockDim.x) {
+    double ss = __ldcg(so5 + f);
+    so5[f] = 0.0;
+    if (bias) ss -= bsum;
+    const double c = __ldcg(co5 + f);
+    co5[f] = 0.0;  // Co5 may have been scattered (staging pass): re-arm it too
+    double den = fabs(c);
+    if (den < fabs(ss)) den = fabs(ss);
+    if (den < 1.0) den = 1.0;
+    const double dev = fabs(c - ss) / den;
+    if (dev == dev && dev > 0.0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(dev);
+      devb = b > devb ? b : devb;
+    }
+    bad += values_differ_guarded(c, ss, tau) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, devb, o);
+    devb = other > devb ? other : devb;
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_bad[w] = bad;
+    s_dev[w] = devb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int fl = 0;
+    unsigned long long mb = 0ull;
+    for (int k = 0; k < nw; ++k) {
+      fl += s_bad[k];
+      mb = s_dev[k] > mb ? s_dev[k] : mb;
+    }
+    volatile DetectStats* h = host_out;
+    h->flagged = fl;
+    h->max_rel_dev_bits = mb;
+    __threadfence_system();
+  }
+}
+
 __global__ void __launch_bounds__(256) k_detect_fused(double* __restrict__ co5, double* __restrict__ so5,
                                                      int N, int E2, int bias, const double* agg, double tau,
                                                      DetectStats* st, unsigned int* ticket, DetectStats* host_out) {
@@ -831,6 +889,12 @@ int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double*
 
 int launch_detect_fused(double* co5, double* so5, int N, int E2, int bias, const double* agg, double tau,
                         DetectStats* st, unsigned int* ticket, DetectStats* host_out, cudaStream_t s) {
+  static const bool one_block = getenv("FTC_DETECT_1BLOCK") != nullptr;  // experiment: slower (see above)
+  if (one_block && E2 <= kDetect1Max) {
+    FTC_LAUNCH_PDL(k_detect_fused1, dim3(1), dim3(1024), 0, s, co5, so5, N, E2, bias, agg, tau, host_out);
+    FTC_CUDA_CHECK(cudaGetLastError());
+    return FTC_OK;
+  }
   FTC_LAUNCH_PDL(k_detect_fused, dim3(blocks_for(E2)), dim3(kThreads), 0, s, co5, so5, N, E2, bias, agg, tau, st, ticket,
                  host_out);
   FTC_CUDA_CHECK(cudaGetLastError());

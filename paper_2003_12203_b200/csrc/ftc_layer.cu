@@ -1116,10 +1116,13 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
       const bool stage = tc_im2col(L->tc) && !(L->nhwc_ready && L->D_staged == D);
       if (stage && d.N <= 32) {
         // small batch: one pass writes the NHWC copy, the exact-order Cd1/Cd2 and, by
-        // linearity, Co5 (each block scatters its Cd1 elements' share)
+        // linearity, Co5 (each block scatters its Cd1 elements' share) -- unless Co5 fits
+        // in the conv's checksum warp (FTC_CO5_IN=1 forces that: experiments)
+        static const bool co5_force = getenv_flag("FTC_CO5_IN");
         const Co5Job job{L->co5f, L->cw1, d.H, d.R, d.stride, d.pad, L->E};
-        CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s, &job));
-        co5_ready = true;
+        CK(launch_nhwc_cd(D, tc_nhwc_buffer(L->tc), d.C, d.H * d.H, 0, d.N, L->cd1, L->cd2, s,
+                          co5_force ? nullptr : &job));
+        co5_ready = !co5_force;
         dt_ready = true;
         cd1_use = L->cd1;
         L->ck_exact = true;
@@ -1138,7 +1141,7 @@ static int launch_impl(ftc_layer* L, const ftc_plan* plan, const float* D, float
     }
     // Co5 in the conv's checksum warp when it fits in the conv's shadow, else in the
     // CoC-D kernel after the conv (one launch either way)
-    const bool co5_in = !co5_ready && tc_co5_in_kernel(L->tc, d.N, L->E);
+    const bool co5_in = !co5_ready && (tc_co5_in_kernel(L->tc, d.N, L->E) || getenv_flag("FTC_CO5_IN"));
     FusedDetect fd{L->co5f, L->so5acc, L->agg, plan->tau, d.bias_enabled ? 1 : 0, L->fstats, L->fticket,
                    L->fstats_hd, co5_in ? cd1_use : nullptr, L->co5tab};
     // the staging pass / conv scatter into the Co5 and So5 accumulators, which only
