@@ -868,19 +868,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       float* op = a.O + ((long long)n * a.M + m0) * E2 + f;
       const float* bp = a.bias ? a.bias + m0 : nullptr;
       if (!slow) {
+        // the FP64 row sums only where someone reads them: So5 (rs) for the fused
+        // CoC-D, both sums for the row-sum slabs; the plain conv stores only (3 FP64 ops
+        // per output were a third of a 1-chunk tile's epilogue, VGG c1)
+        const int sums = a.rowsum ? 2 : (FUSE ? 1 : 0);
         if (valid) {
-          if (bp) {
+          if (sums == 0) {
+#pragma unroll
+            for (int jj = 0; jj < HALF; ++jj) op[jj * E2] = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
+          } else if (sums == 1) {
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) {
-              const float val = (float)sum[jj] + __ldg(bp + jj);
+              const float val = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
               op[jj * E2] = val;
               rs = dadd(rs, (double)val);
-              rsm = dadd(rsm, dmul((double)(m0 + jj), (double)val));
             }
           } else {
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) {
-              const float val = (float)sum[jj];
+              const float val = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
               op[jj * E2] = val;
               rs = dadd(rs, (double)val);
               rsm = dadd(rsm, dmul((double)(m0 + jj), (double)val));
