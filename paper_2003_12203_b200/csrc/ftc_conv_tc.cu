@@ -204,6 +204,40 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// CTA-pair B multicast (CL = 2): one half of a B stage lands in both CTAs of the cluster
+// at the same shared-memory offset and signals the same barrier offset in each
+__device__ __forceinline__ void bulk_g2s_mc2(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_peer(uint32_t bar, uint32_t peer) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(bar), "r"(peer));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster_lazy(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // im2col TMA: 128 consecutive output pixels (starting at input position (n, h, w) of the
 // bounding-box traversal) x channels [c, c+32) at filter tap (oh, ow)
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
@@ -292,6 +326,30 @@ __device__ __forceinline__ float tf32_rn(float v) {
   return __uint_as_float(r);
 }
 
+// v = hi + lo: hi = RN_tf32(v) in integer arithmetic (the tensor core reads the top 19
+// bits), lo = v - hi exact in FP32, rounded the same way.  FTC_SPLIT_MODE 1 (experiment):
+// lo handed over unrounded (the tensor core ignores the low 13 bits: a truncation of lo,
+// 2^-22 |v|, the size of the dropped lo*lo term); 2: cvt.rna.tf32 for both roundings.
+#ifndef FTC_SPLIT_MODE
+#define FTC_SPLIT_MODE 0
+#endif
+__device__ __forceinline__ void split_tf32(uint32_t v, uint32_t& hi, uint32_t& lo) {
+#if FTC_SPLIT_MODE == 2
+  const float h = tf32_rn(__uint_as_float(v));
+  hi = __float_as_uint(h);
+  lo = __float_as_uint(tf32_rn(__uint_as_float(v) - h));
+#else
+  const uint32_t h = (v + 0x1000u) & 0xFFFFE000u;
+  hi = h;
+  const float l = __uint_as_float(v) - __uint_as_float(h);
+#if FTC_SPLIT_MODE == 1
+  lo = __float_as_uint(l);
+#else
+  lo = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
+#endif
+#endif
+}
+
 // ------------------------------------------------------------------ kernel
 // Out of line: the store loop is unrolled over every column of the tile and an inlined
 // fault loop + mask lookup per column made the epilogue ~200 KB of SASS (instruction-
@@ -323,8 +381,14 @@ __device__ __noinline__ HookOut epilogue_hooks(float v, int n, int m, int x, int
 // chunk); 2: TMA im2col into shared memory, producers only split and store to TMEM.
 // FUSE: clean-path CoC-D operands inside the kernel: the checksum warp computes Co5, the
 // epilogue adds its row sums into So5; launch_detect_fused compares them afterwards.
-template <int BN, int MODE, bool FUSE, bool GROUPED>
+// CL = 2: CTA pairs (cluster of 2) take the two pixel tiles (2k, 2k+1) of one N-tile in
+// lockstep and share the B stream: each loader fetches half of every B stage and
+// multicasts it into both CTAs (L2 -> SM traffic per chunk 48 -> 32 KB at BN = 128; the
+// long-K layers ran at ~85% of the L2 throughput cap).  MODE 2, full pixel range only;
+// an odd tile count gives the last pair a phantom tile (p >= P: computed, never stored).
+template <int BN, int MODE, bool FUSE, bool GROUPED, int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_constant__ CUtensorMap tmA) {
+  static_assert(CL == 1 || (CL == 2 && MODE == 2 && !GROUPED && kOneCommit), "CTA-pair mode: TMA im2col layers");
   constexpr bool NHWC = MODE == 1;
   constexpr bool TMAA = MODE >= 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -392,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
   }
   tc_before();
   __syncthreads();
+  if (CL == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / multicast
   tc_after();
   const uint32_t tmem = *tmem_slot;
   // PDL: the prologue above overlapped the previous kernel's tail; the next kernel (the
@@ -449,12 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           if (lane == 0) mbar_arrive(emptyAs0 + 8 * sa_c);
           uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint32_t h = (v[e] + 0x1000u) & 0xFFFFE000u;
-            hi[e] = h;
-            const float l = __uint_as_float(v[e]) - __uint_as_float(h);
-            lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
-          }
+          for (int e = 0; e < 16; ++e) split_tf32(v[e], hi[e], lo[e]);
           if (!kOneCommit) mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
           else if (g >= (uint32_t)kSA) gdone_wait(gdone0, jprev, false);
           if (warp == 0) TC_TRACE(pprof2, 1, g);
@@ -553,14 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         }
         uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          // round-to-nearest TF32 in integer arithmetic (the tensor core reads the
-          // top 19 bits), lo = v - hi exact in FP32, rounded the same way
-          const uint32_t h = (__float_as_uint(v[e]) + 0x1000u) & 0xFFFFE000u;
-          hi[e] = h;
-          const float l = v[e] - __uint_as_float(h);
-          lo[e] = (__float_as_uint(l) + 0x1000u) & 0xFFFFE000u;
-        }
+        for (int e = 0; e < 16; ++e) split_tf32(__float_as_uint(v[e]), hi[e], lo[e]);
         if (warp == 0) TC_TRACE(pprof, 0, g);
         if (!kOneCommit) mbar_wait(emptyA0 + 8 * s, ph ^ 1u);
         else if (g >= (uint32_t)kSA) gdone_wait(gdone0, jprev, false);
@@ -588,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
     const bool doA = TMAA && (kSplitLoader ? lane == 1 : lane == 0);
     if (doA || doB) {
       uint32_t g = 0, sB = 0, phB = 0, sa = 0, pha = 0;
+      const uint32_t crank = CL == 2 ? cluster_ctarank() : 0u;
       const int ncb = (GROUPED ? a.Ckw : a.C) / 32;
       const uint32_t ngtl = (uint32_t)(a.nkc + kG - 1) / (uint32_t)kG;
       uint32_t jb[4] = {0, 0, 0, 0}, tll = 0;  // groups of the last 4 chunks (kOneCommit)
@@ -596,7 +650,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         const int cg = GROUPED ? nt / a.ntg * a.Ckw : 0;  // the tile's group's first channel
         const float* src = a.Wp + (long long)nt * a.nkc * 2 * BN * kBK;
         // MODE 2: the tile's first output pixel, as a TMA im2col traversal start
-        const long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
+        long long p0 = (long long)(a.pt_lo + t % a.npt) * kBM;
+        if (CL == 2 && p0 >= a.P) p0 = 0;  // phantom tile of an odd pair: any in-range pixels
         const int n0 = (int)(p0 / E2), f0 = (int)(p0 % E2);
         const int cw = (f0 % E) * a.U - a.pad, ch = (f0 / E) * a.U - a.pad;
         if (MODE == 0 && doB) {
@@ -651,9 +706,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
           jb[0] = tll * ngtl + (uint32_t)kc / (uint32_t)kG;
           if (!kOneCommit) mbar_wait_lazy(emptyB0 + 8 * s, ph ^ 1u);
           else if (g >= (uint32_t)SB) gdone_wait(gdone0, jprev, true);
+          if (CL == 2 && g >= (uint32_t)SB) {
+            // this CTA has consumed the stage's previous use: tell the peer (its half goes
+            // into this CTA's stage too) and wait for the peer's consumption likewise
+            mbar_arrive_peer(emptyB0 + 8 * s, crank ^ 1u);
+            mbar_wait_cluster_lazy(emptyB0 + 8 * s, ph ^ 1u);
+          }
           TC_TRACE((a.dbg & 64) && blockIdx.x == 0, 8, g);
           if (a.dbg & 16) {
             mbar_arrive(fullB0 + 8 * s);
+          } else if (CL == 2) {
+            // rank 0 fetches the hi tile, rank 1 the lo tile, each into both CTAs
+            const uint32_t hb = stage_bytes / 2u;
+            mbar_arrive_expect_tx(fullB0 + 8 * s, stage_bytes);
+            bulk_g2s_mc2(sbase + s * stage_bytes + crank * hb,
+                         reinterpret_cast<const uint8_t*>(src + (long long)kc * 2 * BN * kBK) + crank * hb, hb,
+                         fullB0 + 8 * s);
           } else {
             mbar_arrive_expect_tx(fullB0 + 8 * s, stage_bytes);
             bulk_g2s(sbase + s * stage_bytes, src + (long long)kc * 2 * BN * kBK, stage_bytes, fullB0 + 8 * s);
@@ -946,6 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
   }
   tc_before();
   __syncthreads();
+  if (CL == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   tc_after();
   if ((a.dbg & 64) && blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t0 = g_tc_trace[4][0];
@@ -1181,6 +1250,44 @@ int launch_bn(const TcArgs& a, const CUtensorMap& tm, int grid, size_t smem, cud
     attr_set[dev] = true;
   }
   FTC_LAUNCH_PDL(k_conv_tc<BN, MODE, FUSE, GROUPED>, dim3(grid), dim3(kThreads), smem, s, a, tm);
+  FTC_CUDA_CHECK(cudaGetLastError());
+  return FTC_OK;
+}
+
+// CTA-pair launch (cluster of 2, B multicast): grid = 2 x the co-resident cluster count
+template <int BN, bool FUSE>
+int launch_cl2(const TcArgs& a, const CUtensorMap& tm, int tiles, size_t smem, cudaStream_t s) {
+  static bool attr_set[kMaxDevices] = {false};
+  static int max_clusters[kMaxDevices] = {0};
+  const int dev = current_device();
+  auto k = k_conv_tc<BN, 2, FUSE, false, 2>;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  if (!attr_set[dev]) {
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    cfg.gridDim = dim3((unsigned)(num_sms(dev) & ~1));
+    int nc = 0;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess || nc < 1) nc = num_sms(dev) / 2;
+    cfg.numAttrs = 2;
+    max_clusters[dev] = nc;
+    attr_set[dev] = true;
+  }
+  const int cap = 2 * max_clusters[dev];
+  cfg.gridDim = dim3((unsigned)(tiles < cap ? tiles : cap));
+  FTC_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, a, tm));
+  count_launch();
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }
@@ -1433,6 +1540,17 @@ int conv_tc_launch(const TcPlan* p, const ConvArgs& c, cudaStream_t s) {
       return FTC_CONFIG_ERROR;
     }
     a.fd = *c.fd;
+  }
+  // CTA pairs sharing the B stream (k_conv_tc<..., CL = 2>): TMA im2col layers over the
+  // full pixel range with enough tiles for every pair
+  static const int cl_mode = getenv("FTC_TC_CL") ? atoi(getenv("FTC_TC_CL")) : 0;
+  if (cl_mode == 2 && p->im2col && p->groups == 1 && a.pt_lo == 0 && p_hi == a.P && (p->BN == 64 || p->BN == 128) &&
+      tiles >= 2 * n_sms) {
+    a.npt = (a.npt + 1) & ~1;
+    const int tiles2 = a.ntiles * a.npt;
+    if (p->BN == 128)
+      return fuse ? launch_cl2<128, true>(a, p->tmA, tiles2, smem, s) : launch_cl2<128, false>(a, p->tmA, tiles2, smem, s);
+    return fuse ? launch_cl2<64, true>(a, p->tmA, tiles2, smem, s) : launch_cl2<64, false>(a, p->tmA, tiles2, smem, s);
   }
 #define FTC_BN_SWITCH(MODE, FUSE)                                                            \
   switch (p->BN) {                                                                           \

@@ -38,8 +38,8 @@ def main(rep, flops=None):
               "ns": 1e-3, "us": 1, "ms": 1e3}
         return sc.get(u, 1) / to
 
-    print("| # | kernel | time us | DRAM read MB | DRAM write MB | L2->SM sectors (M) | L1 hit % | tensor pipe active % | issue active % | regs |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+    print("| # | kernel | time us | DRAM read MB | DRAM write MB | L2->SM sectors (M) | L2 throughput % (ncu peak) | L1 hit % | tensor pipe active % | issue active % | regs |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|")
     tot_t = tot_b = 0.0
     for k, d in enumerate(data):
         name = d[col["Kernel Name"]].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
@@ -47,6 +47,7 @@ def main(rep, flops=None):
         rd = g(d, "dram__bytes_read.sum") * unit_scale("dram__bytes_read.sum", 1e6)
         wr = g(d, "dram__bytes_write.sum") * unit_scale("dram__bytes_write.sum", 1e6)
         l2 = g(d, "lts__t_sectors_srcunit_tex_op_read.sum") / 1e6
+        l2p = g(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed")
         l1 = g(d, "l1tex__t_sector_hit_rate.pct")
         tp = g(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
         if tp != tp:
@@ -55,7 +56,7 @@ def main(rep, flops=None):
         regs = g(d, "launch__registers_per_thread")
         tot_t += t
         tot_b += rd + wr
-        print(f"| {k} | {name} | {t:.1f} | {rd:.1f} | {wr:.1f} | {l2:.1f} | {l1:.1f} | {tp:.1f} | {ia:.1f} | {regs:.0f} |")
+        print(f"| {k} | {name} | {t:.1f} | {rd:.1f} | {wr:.1f} | {l2:.1f} | {l2p:.1f} | {l1:.1f} | {tp:.1f} | {ia:.1f} | {regs:.0f} |")
     print(f"\nSum: {tot_t:.1f} us, DRAM {tot_b:.1f} MB (read+write)")
     if flops:
         print(f"useful FLOPs {float(flops):.4e} -> {float(flops) / (tot_t * 1e-6) / 1e12:.1f} TF/s under ncu")
