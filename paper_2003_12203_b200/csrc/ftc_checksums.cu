@@ -659,13 +659,30 @@ __global__ void __launch_bounds__(256) k_co5_detect(const double* __restrict__ c
     for (int c = sl; c < C; c += S) {
       const double* src = cd1 + (long long)c * H * H;
       const double* ker = cw1 + c * RR;
-      for (int i = 0; i < R; ++i) {
-        const int hh = hb + i;
-        if (hh < 0 || hh >= H) continue;
-        for (int j = 0; j < R; ++j) {
-          const int ww = wb + j;
-          if (ww < 0 || ww >= H) continue;
-          c5 = fma(__ldg(src + hh * H + ww), __ldg(ker + i * R + j), c5);
+      if constexpr (RT > 0) {
+        // the window's loads issued together (predicated, no branches between them):
+        // after the large layers' conv this kernel is exposed, one L2 round trip per
+        // channel instead of one per tap
+        double v[RT * RT], w[RT * RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+          for (int j = 0; j < RT; ++j) {
+            const bool ok = (unsigned)(hb + i) < (unsigned)H && (unsigned)(wb + j) < (unsigned)H;
+            v[i * RT + j] = ok ? __ldg(src + (hb + i) * H + wb + j) : 0.0;
+            w[i * RT + j] = __ldg(ker + i * RT + j);
+          }
+#pragma unroll
+        for (int q = 0; q < RT * RT; ++q) c5 = fma(v[q], w[q], c5);
+      } else {
+        for (int i = 0; i < R; ++i) {
+          const int hh = hb + i;
+          if (hh < 0 || hh >= H) continue;
+          for (int j = 0; j < R; ++j) {
+            const int ww = wb + j;
+            if (ww < 0 || ww >= H) continue;
+            c5 = fma(__ldg(src + hh * H + ww), __ldg(ker + i * R + j), c5);
+          }
         }
       }
     }
@@ -877,12 +894,16 @@ int launch_co5_detect(const double* cd1, const double* cw1, double* co5, double*
   int P = 32;
   while (P > 1 && (E2 + P - 1) / P < 2 * 148 * 4 && 256 / P < C) P >>= 1;
   const int g = (E2 + P - 1) / P;
-  if (R == 3)
-    FTC_LAUNCH_PDL(k_co5_detect<3>, dim3(g), dim3(256), 0, s, cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg,
-                   tau, st, ticket, host_out);
-  else
-    FTC_LAUNCH_PDL(k_co5_detect<0>, dim3(g), dim3(256), 0, s, cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg,
-                   tau, st, ticket, host_out);
+#define FTC_C5D(RT)                                                                                                  \
+  FTC_LAUNCH_PDL(k_co5_detect<RT>, dim3(g), dim3(256), 0, s, cd1, cw1, co5, so5, N, C, H, R, U, pad, E, P, bias, agg, \
+                 tau, st, ticket, host_out)
+  switch (R) {
+    case 1: FTC_C5D(1); break;
+    case 3: FTC_C5D(3); break;
+    case 5: FTC_C5D(5); break;
+    default: FTC_C5D(0); break;
+  }
+#undef FTC_C5D
   FTC_CUDA_CHECK(cudaGetLastError());
   return FTC_OK;
 }

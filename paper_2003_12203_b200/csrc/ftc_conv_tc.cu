@@ -883,8 +883,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
       const int pt = a.pt_lo + t % a.npt;
       const long long p = (long long)pt * kBM + r;
       const bool valid = p < a.P;
-      const int n = valid ? (int)(p / E2) : 0;
-      const int f = valid ? (int)(p % E2) : 0;
+      // P < 2^31 (tc_supported): 32-bit divisions (the 64-bit ones sat between a tile's
+      // store and the next tile's first drain)
+      const unsigned pu = valid ? (unsigned)p : 0u;
+      const int n = (int)(pu / (unsigned)E2);
+      const int f = (int)(pu - (unsigned)n * (unsigned)E2);
       const int x = f / E, y = f - (f / E) * E;
       // running sums of the group partials, in group order, in FP32 (several times closer
       // to the exact conv than the reference's sequential FP32 loop; FP64 sums for the
@@ -945,12 +948,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) op[jj * E2] = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
           } else if (sums == 1) {
+            // So5 row sum as an error-free FP32 accumulation (TwoSum: s1 + e1 carries the
+            // sum to ~2^-46 of the terms' magnitude; the screen's guard band is 1e-3 of
+            // tau) and two conversions per thread: a cvt.f64.f32 + DADD per output ran at
+            // ~6 conversions per clock per SM, 2.7K cycles of a 6K-cycle tile end that
+            // the issuers wait on (r02ce traces)
+            float s1 = 0.f, e1 = 0.f;
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) {
               const float val = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
               op[jj * E2] = val;
-              rs = dadd(rs, (double)val);
+              const float t = __fadd_rn(s1, val);
+              const float bb = __fsub_rn(t, s1);
+              e1 = __fadd_rn(e1, __fadd_rn(__fsub_rn(s1, __fsub_rn(t, bb)), __fsub_rn(val, bb)));
+              s1 = t;
             }
+            rs = dadd((double)s1, (double)e1);
           } else {
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) {
@@ -1439,7 +1452,12 @@ bool tc_co5_in_kernel(const TcPlan* p, int N, int E) {
   const long long rounds = pos * ((Kc + 32LL * kCkUnroll - 1) / (32LL * kCkUnroll));
   const long long tiles = ((long long)N * E2 + kBM - 1) / kBM * p->ntiles;
   const long long conv = (tiles + grid - 1) / grid * p->nkc * 1000LL;
-  return rounds * 700LL * 4 <= conv;
+  // a round is two dependent loads (tap entry, then Cd1) through an L2 the conv keeps
+  // ~85% busy: measured ~7,300 cycles (VGG-19 c4: the checksum warp finished 0.55 ms after
+  // the MMAs, c3 / c2 75-85 us; r02cc ncu lists).  Layers that do not fit take Co5 in the
+  // CoC-D kernel after the conv instead.
+  static const long long round_cycles = getenv("FTC_CO5_ROUND") ? atoll(getenv("FTC_CO5_ROUND")) : 8000LL;
+  return rounds * round_cycles <= conv;
 }
 float* tc_nhwc_buffer(const TcPlan* p) { return p ? p->Dt : nullptr; }
 

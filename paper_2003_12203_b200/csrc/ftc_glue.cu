@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
 // POOL2: 2x2 stride-2 max-pool after the activation (Ho % 4 == 0, so a thread's 4
 // output positions share a row and read two rows of 8 inputs: four 16-byte loads).
 constexpr int kV4Img = 4;
-template <int ACT, bool POOL2, bool VEC = true>
+// CD1 = false: the same pass without the checksum (the unprotected net's glue, so that the
+// ABFT overhead is measured against equally tuned kernels).
+template <int ACT, bool POOL2, bool VEC = true, bool CD1 = true>
 __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in, float* __restrict__ out,
                                                    float* __restrict__ out_t, int N, int NG, int C, int HW,
                                                    double* __restrict__ ws, long long tick_off, long long slab_off,
@@ -232,10 +234,12 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
       if (ok && u < cnt) {
         if (VEC) {
           if (op) op[u * step4] = v[u];
-          acc[0] += (double)v[u].x;
-          acc[1] += (double)v[u].y;
-          acc[2] += (double)v[u].z;
-          acc[3] += (double)v[u].w;
+          if (CD1) {
+            acc[0] += (double)v[u].x;
+            acc[1] += (double)v[u].y;
+            acc[2] += (double)v[u].z;
+            acc[3] += (double)v[u].w;
+          }
         } else {
           const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
           float* of = out ? out + ((long long)(n + u) * C + c) * HW + pos : nullptr;  // element addressing
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
           for (int q = 0; q < 4; ++q)
             if (q < nq) {
               if (of) of[q] = e4[q];
-              acc[q] += (double)e4[q];
+              if (CD1) acc[q] += (double)e4[q];
             }
         }
       }
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
     if (op) op += kV4Img * step4;
   }
   pdl_trigger();
+  if constexpr (!CD1) return;
   const long long per = plane_c;
   const long long e = (long long)c * HW + pos;
   if (ok) {
@@ -620,9 +625,15 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
     // for, and no more image groups than it holds
     const int HW = Ho * Ho;
     const dim3 gv((unsigned)((HW + 31) / 32), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
-#define FTC_V4(A, P)                                                                                              \
-  FTC_LAUNCH_PDL((k_act_v4_cd1<A, P>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws, w.tick_off, w.slab_off, \
-                 Ho)
+#define FTC_V4(A, P)                                                                                           \
+  do {                                                                                                         \
+    if (ws)                                                                                                    \
+      FTC_LAUNCH_PDL((k_act_v4_cd1<A, P>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws, w.tick_off,    \
+                     w.slab_off, Ho);                                                                          \
+    else                                                                                                       \
+      FTC_LAUNCH_PDL((k_act_v4_cd1<A, P, true, false>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws,  \
+                     w.tick_off, w.slab_off, Ho);                                                              \
+  } while (0)
     if (pool2) {
       if (act == 1) FTC_V4(1, true);
       else if (act == 2) FTC_V4(2, true);
@@ -632,9 +643,15 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
       else if (act == 2) FTC_V4(2, false);
       else FTC_V4(0, false);
     } else {
-#define FTC_V1(A)                                                                                                  \
-  FTC_LAUNCH_PDL((k_act_v4_cd1<A, false, false>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws, w.tick_off, \
-                 w.slab_off, Ho)
+#define FTC_V1(A)                                                                                               \
+  do {                                                                                                          \
+    if (ws)                                                                                                     \
+      FTC_LAUNCH_PDL((k_act_v4_cd1<A, false, false>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, ws,      \
+                     w.tick_off, w.slab_off, Ho);                                                               \
+    else                                                                                                        \
+      FTC_LAUNCH_PDL((k_act_v4_cd1<A, false, false, false>), gv, dim3(256), 0, st, in, out, out_t, N, NG, C, HW, \
+                     ws, w.tick_off, w.slab_off, Ho);                                                           \
+  } while (0)
       if (act == 1) FTC_V1(1);
       else if (act == 2) FTC_V1(2);
       else FTC_V1(0);
@@ -644,6 +661,9 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
     FTC_CUDA_CHECK(cudaGetLastError());
     return FTC_OK;
   }
+  if (!ws)
+    return out_t ? launch_act_pool_nhwc(in, out, out_t, N, C, H, act, k, s, p, st)
+                 : launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
   const dim3 g((unsigned)((Ho * Ho + 7) / 8), (unsigned)(C / 32), (unsigned)((N + NG - 1) / NG));
 #define FTC_APT2(KT, ACT) \
   FTC_LAUNCH_PDL(k_act_pool_t_cd1<KT, ACT>, g, dim3(256), 0, st, in, out, out_t, N, NG, C, H, k, s, p, Ho, ws, \
@@ -733,8 +753,11 @@ int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t 
   cudaStream_t st = (cudaStream_t)stream;
   const int Ho = (H + 2 * p - k) / s + 1;
   if (!ws) {
-    return out_nhwc ? launch_act_pool_nhwc(in, out, out_nhwc, N, C, H, act, k, s, p, st)
-                    : launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
+    // no checksum (unprotected nets): the same tuned pass without the Cd1 sums when it
+    // writes an NHWC copy, else the plain kernels
+    return (out_nhwc && C % 32 == 0) ? launch_act_pool_nhwc_cd1(in, out, out_nhwc, N, C, H, act, k, s, p, nullptr, st)
+           : out_nhwc                ? launch_act_pool_nhwc(in, out, out_nhwc, N, C, H, act, k, s, p, st)
+                                     : launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
   }
   // with the consumer's Cd1: channel-blocked kernel looping over image groups (one
   // pass), or -- C not a multiple of 32 -- act + pool, then Cd1 from the L2-hot output

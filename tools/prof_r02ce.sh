@@ -1,0 +1,8 @@
+set -x
+timeout 300 python tools/tc_trace3.py > gpurun_out/r02ce_trace_c3.log 2>&1
+TRACE_PROT=1 timeout 300 python tools/tc_trace3.py > gpurun_out/r02ce_trace_c3p.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r02ce_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02ce_pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/r02ce_bench.json 2> gpurun_out/r02ce_bench.err
+M="--metrics gpu__time_duration.sum --clock-control none --csv"
+timeout 900 ncu $M -k regex:"k_conv_tc|k_co5|k_detect" --log-file gpurun_out/r02ce_diag.csv python tools/c4_diag2.py > gpurun_out/r02ce_diag.log 2>&1
+echo done
