@@ -332,6 +332,169 @@ __global__ void __launch_bounds__(32 * kSeqWarps) k_seq_sums567(VirtualO v, int 
   out[f] = s;
 }
 
+// So5/So6/So7, staged form: a block owns 32 positions.  Warp 0 is the chain warp, a lane
+// per position running its three chains (s5, s6, s7: three independent DADDs per term, so
+// the add latency is covered and the FP64 issue rate sets the pace); warps 1-7 stage the
+// terms ahead of it: coalesced loads of O (lane = position), the verifier's FP64
+// overrides, the exact products m*x and n*x, written as FP64 rows [family][term][32
+// positions] into a double-buffered shared-memory tile.  The loaders hold the tile after
+// next in registers, so a load has a whole chain tile (~1.2K cycles) to land.  Same
+// operations in the same order as k_seq_sums567 (n outer, m inner; x, m*x, n*x exact
+// products, one DADD each), hence bitwise the same sums, at ~23 cycles per term instead
+// of ~50 (one chain per warp fed by shuffles): AlexNet conv2 So5-7 877 -> 393 us.
+constexpr int kStT = 128;        // terms per staged tile
+constexpr int kStLW = 12;            // loader warps: warps 1-15 of the block except 4, 8, 12 -- the chain warp's
+                                     // scheduler (sub-partition 0) issues for nobody else (with loaders beside it the
+                                     // chain warp got every fourth issue slot: ~32 cycles per term)
+constexpr int kStLoad = kStLW * 32;  // loader threads
+constexpr int kStPer = (kStT * 32 + kStLoad - 1) / kStLoad;  // elements per loader thread and tile
+template <bool VIRT>
+__global__ void __launch_bounds__(512) k_seq_sums567_staged(VirtualO v, int N, int M, int E2,
+                                                          const int* __restrict__ list,
+                                                          const int* __restrict__ count, const double* agg,
+                                                          double* __restrict__ so5, double* __restrict__ so6,
+                                                          double* __restrict__ so7) {
+  extern __shared__ double st_tile[];  // [2][3][kStT][32]
+  const int npos = list ? *count : E2;
+  const int p0 = blockIdx.x * 32;
+  if (p0 >= npos) return;  // whole block
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long NM = (long long)N * M;
+  const int ntile = (int)((NM + kStT - 1) / kStT);
+  const int pl = p0 + lane;
+  const bool pok = pl < npos;
+  const int f = pok ? (list ? list[pl] : pl) : 0;
+  // loader state: element e = li + kStLoad * j of a tile is (term e / 32, position e % 32);
+  // a warp's lanes share the term and cover the 32 positions.  Two tiles of loads are in
+  // flight in registers (fetched two barriers before they are stashed), and the weights
+  // (double)m, (double)n advance incrementally (a term step of kStLW per element): no integer
+  // division or int -> FP64 conversion per element.
+  const bool loader = (warp & 3) != 0;
+  const int li = ((warp >> 2) * 3 + (warp & 3) - 1) * 32 + lane;  // loaders: 0 .. kStLoad - 1
+  float xr[2][kStPer];
+  uint8_t pr[2][kStPer];
+  // element j of a tile: term row tr + kStLW j (tr = li / 32), valid rows < kStT -- only
+  // j = kStPer - 1 can fall off the tile (rows 126, 127 exist for tr < 2)
+  const int tr = li >> 5;
+  const long long step = (long long)kStLW * E2;
+  // loads are unconditional: lanes without a position read lane 0's (f = 0 region is
+  // valid memory; their sums are never written), and rows past N*M in the last tile are
+  // clamped to the last term (the chain never reads those rows)
+  auto fetch = [&](int tile, int rs) {
+    const long long q0 = (long long)tile * kStT + tr;
+    if ((long long)(tile + 1) * kStT <= NM) {
+      const float* src = v.O + q0 * E2 + f;
+      const uint8_t* psrc = VIRT ? v.present + q0 * E2 + f : nullptr;
+#pragma unroll
+      for (int j = 0; j < kStPer - 1; ++j) {
+        xr[rs][j] = __ldg(src);
+        if (VIRT) pr[rs][j] = __ldg(psrc);
+        src += step;
+        if (VIRT) psrc += step;
+      }
+      if (tr < kStT - kStLW * (kStPer - 1)) {
+        xr[rs][kStPer - 1] = __ldg(src);
+        if (VIRT) pr[rs][kStPer - 1] = __ldg(psrc);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kStPer; ++j) {
+        const long long q = min(q0 + kStLW * j, NM - 1);
+        xr[rs][j] = __ldg(v.O + q * E2 + f);
+        if (VIRT) pr[rs][j] = __ldg(v.present + q * E2 + f);
+      }
+    }
+  };
+  const double dM = (double)M;
+  auto stash = [&](int tile, int b, int rs) {
+    double* t5 = st_tile + (size_t)b * 3 * kStT * 32 + li;
+    const unsigned q0 = (unsigned)tile * kStT + (unsigned)tr;
+    const unsigned n0 = q0 / (unsigned)M;
+    double dn = (double)n0, dm = (double)(q0 - n0 * (unsigned)M);
+#pragma unroll
+    for (int j = 0; j < kStPer; ++j) {
+      if (j < kStPer - 1 || tr < kStT - kStLW * (kStPer - 1)) {
+        double x = (double)xr[rs][j];
+        if (VIRT && pr[rs][j]) x = __ldg(v.ov + min((long long)q0 + kStLW * j, NM - 1) * E2 + f);
+        t5[kStLoad * j] = x;  // rows past N*M hold values the chain never reads
+        t5[kStLoad * j + kStT * 32] = dmul(dm, x);
+        t5[kStLoad * j + 2 * kStT * 32] = dmul(dn, x);
+      }
+      dm += (double)kStLW;  // exact small integers in FP64; M >= kStLW (launcher), so one wrap at most
+      if (dm >= dM) {
+        dm -= dM;
+        dn += 1.0;
+      }
+    }
+  };
+  if (loader) {
+    fetch(0, 0);
+    if (ntile > 1) fetch(1, 1);
+    stash(0, 0, 0);
+    if (ntile > 2) fetch(2, 0);
+  }
+  __syncthreads();
+  double s5 = 0.0, s6 = 0.0, s7 = 0.0;
+  for (int k = 0; k < ntile; ++k) {
+    if (loader) {
+      // tile k+1 sits in register set (k+1)&1 (fetched an iteration ago); once stashed,
+      // that set takes tile k+3
+      if (k + 1 < ntile) {
+        if ((k + 1) & 1) {
+          stash(k + 1, 1, 1);
+          if (k + 3 < ntile) fetch(k + 3, 1);
+        } else {
+          stash(k + 1, 0, 0);
+          if (k + 3 < ntile) fetch(k + 3, 0);
+        }
+      }
+    } else if (warp == 0) {
+      const double* t5 = st_tile + (size_t)(k & 1) * 3 * kStT * 32 + lane;
+      const double* t6 = t5 + kStT * 32;
+      const double* t7 = t6 + kStT * 32;
+      const int nt = (int)min((long long)kStT, NM - (long long)k * kStT);
+      int t = 0;
+      // all 24 loads of a batch issue before its adds (volatile asm keeps the order: left
+      // to the compiler the loads were interleaved four at a time with the adds and every
+      // add waited out a shared-memory latency, ~32 cycles per term; a double-buffered
+      // form with the next batch's loads ahead of the current adds measured no faster)
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(t5);
+      for (; t + 8 <= nt; t += 8) {
+        double a[8], b[8], c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t ad = sa + (uint32_t)(t + u) * 256u;
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[u]) : "r"(ad));
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(b[u]) : "r"(ad + (uint32_t)kStT * 256u));
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(c[u]) : "r"(ad + 2u * (uint32_t)kStT * 256u));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(s5) : "d"(a[u]));
+          asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(s6) : "d"(b[u]));
+          asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(s7) : "d"(c[u]));
+        }
+      }
+      for (; t < nt; ++t) {
+        s5 = dadd(s5, t5[t * 32]);
+        s6 = dadd(s6, t6[t * 32]);
+        s7 = dadd(s7, t7[t * 32]);
+      }
+    }
+    __syncthreads();
+  }
+  if (warp != 0 || !pok) return;
+  if (agg) {  // BiasAdjuster (checksums.hpp:226-235)
+    const double nN = (double)N, wnn = (double)((long long)N * (N - 1) / 2);
+    s5 = dsub(s5, dmul(nN, agg[0]));
+    s6 = dsub(s6, dmul(nN, agg[1]));
+    s7 = dsub(s7, dmul(wnn, agg[0]));
+  }
+  if (so5) so5[f] = s5;
+  if (so6) so6[f] = s6;
+  if (so7) so7[f] = s7;
+}
+
 // ------------------------------------------------------------------ K6: CoC-D
 __device__ __forceinline__ void detect_one(double c, double s, double tau, int* flagged,
                                            unsigned long long* mrd_bits, bool* bad) {
@@ -824,6 +987,22 @@ int launch_bias_aggregates(const float* bias, int M, double* agg, cudaStream_t s
 
 int launch_seq_sums567(const VirtualO& v, int N, int M, int E2, const int* list, const int* count, const double* agg,
                        double* so5, double* so6, double* so7, cudaStream_t s) {
+  // long chains (the error path at batch scale): the staged form, a lane per position fed
+  // by loader warps; short ones keep the warp-per-chain form (more chains in flight)
+  static const bool staged_off = getenv("FTC_SEQ_STAGED") && atoi(getenv("FTC_SEQ_STAGED")) == 0;
+  if (!staged_off && M >= kStLW && (long long)N * M >= 1024 && (long long)N * M < (1LL << 31)) {
+    const size_t smem = (size_t)2 * 3 * kStT * 32 * sizeof(double);
+    // per-device function attribute; the error path is rare, so it is set on every call
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_seq_sums567_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FTC_CUDA_CHECK(cudaFuncSetAttribute(k_seq_sums567_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 gs((unsigned)((E2 + 31) / 32));
+    if (v.present)
+      FTC_LAUNCH(k_seq_sums567_staged<true><<<gs, 512, smem, s>>>(v, N, M, E2, list, count, agg, so5, so6, so7));
+    else
+      FTC_LAUNCH(k_seq_sums567_staged<false><<<gs, 512, smem, s>>>(v, N, M, E2, list, count, agg, so5, so6, so7));
+    FTC_CUDA_CHECK(cudaGetLastError());
+    return FTC_OK;
+  }
   const dim3 g((unsigned)E2);
   if (v.present)
     FTC_LAUNCH(k_seq_sums567<true><<<g, 32 * kSeqWarps, 0, s>>>(v, N, M, E2, list, count, agg, so5, so6, so7, 0));
