@@ -326,6 +326,8 @@ int validate(const ftc_conv_desc* d, int* E) {
 }
 
 // ------------------------------------------------------------------ error path pieces
+bool getenv_flag(const char* name);  // defined below
+
 struct EP {
   ftc_layer* L;
   cudaStream_t s;
@@ -566,8 +568,28 @@ int detect_and_reload(EP& e, ftc_layer_report* rep, int* resolved) {
   // and So7 come with So5: the three chains run side by side in one launch whose time is
   // the chain length, and CoC needs them next (values identical whenever computed: O is
   // unchanged until a scheme patches it)
-  CK(ensure_cs(e, FTC_CK_O5));
-  CK(ensure_s(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+  // The chain-bound So5-7 launch runs on the layer's side stream beside Co5 -- and, ahead
+  // of their use, Co6/Co7 and the kernel checksums of verify_kernel -- on the main one:
+  // all read only D, W, the input checksums and the unpatched O (this path is entered
+  // after the clean-path screen fired, so the exact re-detection nearly always confirms)
+  static const bool ep_serial = getenv_flag("FTC_EP_SERIAL");
+  const bool fork = !ep_serial && L->side && L->ev_start && L->ev_ck;
+  if (fork) {
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, e.s));
+    FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
+    cudaStream_t main_s = e.s;
+    e.s = L->side;
+    const int st_s = ensure_s(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7);
+    e.s = main_s;
+    if (st_s != FTC_OK) return st_s;
+    CK(ensure_cs(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+    CK(launch_kernel_checksums(L->Wcur, d.M, L->Ckw, d.R, d.groups, L->tmp_cw1, L->tmp_cw2, e.s));
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
+    FTC_CUDA_CHECK(cudaStreamWaitEvent(e.s, L->ev_ck, 0));
+  } else {
+    CK(ensure_cs(e, FTC_CK_O5));
+    CK(ensure_s(e, FTC_CK_O5 | FTC_CK_O6 | FTC_CK_O7));
+  }
   bool clean = false;
   double mrd = 0.0;
   CK(detect_exact_clean(e, &clean, &mrd));
@@ -581,7 +603,7 @@ int detect_and_reload(EP& e, ftc_layer_report* rep, int* resolved) {
   }
 
   // verify_kernel (checksums.hpp:250-259) / reload (workflow.hpp:232-245)
-  CK(launch_kernel_checksums(L->Wcur, d.M, L->Ckw, d.R, d.groups, L->tmp_cw1, L->tmp_cw2, e.s));
+  if (!fork) CK(launch_kernel_checksums(L->Wcur, d.M, L->Ckw, d.R, d.groups, L->tmp_cw1, L->tmp_cw2, e.s));
   int kbad = 0;
   CK(count_differ_sync(e, L->tmp_cw1, L->cw1, L->nCw, &kbad));
   if (kbad) {
