@@ -353,6 +353,17 @@ int ensure_cs(EP& e, unsigned want) {
   if (!need) return FTC_OK;
   const ftc_conv_desc& d = L->d;
   const int U = d.stride, p = d.pad, E = L->E;
+  // the weighted family of a pair (Co3 beside Co1 for RC, Co4 beside Co2 for ClC) goes to
+  // the layer's side stream: two independent exact-order FP64 convs of equal length
+  static const bool ep_serial = getenv_flag("FTC_EP_SERIAL");
+  const bool pair = ((need & FTC_CK_O1) && (need & FTC_CK_O3)) || ((need & FTC_CK_O2) && (need & FTC_CK_O4));
+  const bool fork = pair && !ep_serial && L->side && L->ev_start && L->ev_ck;
+  cudaStream_t s2 = e.s;
+  if (fork) {
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_start, e.s));
+    FTC_CUDA_CHECK(cudaStreamWaitEvent(L->side, L->ev_start, 0));
+    s2 = L->side;
+  }
   if (need & FTC_CK_O1)
     CK(launch_conv_f64_exact(L->cd1, true, L->Wcur, false, L->cs[0], 1, d.C, d.H, d.M, L->Ckw, d.R,
                              U, p, d.groups, E, e.s));
@@ -361,10 +372,14 @@ int ensure_cs(EP& e, unsigned want) {
                              U, p, 1, E, e.s));
   if (need & FTC_CK_O3)
     CK(launch_conv_f64_exact(L->cd2, true, L->Wcur, false, L->cs[2], 1, d.C, d.H, d.M, L->Ckw, d.R,
-                             U, p, d.groups, E, e.s));
+                             U, p, d.groups, E, s2));
   if (need & FTC_CK_O4)
     CK(launch_conv_f64_exact(L->Dconv, false, L->cw2, true, L->cs[3], d.N, d.C, d.H, 1, d.C, d.R,
-                             U, p, 1, E, e.s));
+                             U, p, 1, E, s2));
+  if (fork) {
+    FTC_CUDA_CHECK(cudaEventRecord(L->ev_ck, L->side));
+    FTC_CUDA_CHECK(cudaStreamWaitEvent(e.s, L->ev_ck, 0));
+  }
   {  // Co5 / Co6 / Co7: the conv_blocks of (Cd1, Cw1), (Cd1, Cw2), (Cd2, Cw1) in one launch
     const double* ins[3];
     const double* ws[3];
