@@ -186,7 +186,9 @@ def build_workload(name: str, dev, policy: str, shard=None):
     if name == "config1":
         return Config1(dev, shard)
     from paper_2003_12203_b200 import nets
-    return nets.BenchNet(name, dev, policy=policy, shard=shard)
+    # glue outputs read only by a TMA im2col conv skip their NCHW copy (materialised on a
+    # CoC-D detection); FTC_NO_ELIDE=1 writes every activation in both layouts
+    return nets.BenchNet(name, dev, policy=policy, shard=shard, elide_nchw=not os.environ.get("FTC_NO_ELIDE"))
 
 
 def global_batch_of(name: str) -> int:
@@ -616,6 +618,9 @@ def main():
                          "shard": list(shard), "parallelism": f"dp{world} (batch-sharded)",
                          "l2": "flushed (256 MiB write) before every step",
                          "plan": f"rc+clc on, per-layer tau ({args.policy} policy, calibrated per shard)",
+                         "activations": ("glue outputs read by one TMA im2col conv are written channel-last only "
+                                         "(NCHW materialised on a detection)" if not os.environ.get("FTC_NO_ELIDE")
+                                         else "every activation written NCHW + channel-last"),
                          "tau_per_layer": getattr(wl, "taus", None)}
         rec["launches"] = r["launches"]
         rec["steps"] = r["steps"]

@@ -190,6 +190,11 @@ int ftc_protected_conv_host(ftc_layer* layer, const ftc_plan* plan, const float*
 int ftc_protected_conv_launch(ftc_layer* layer, const ftc_plan* plan, const float* D, float* O,
                               const ftc_fault* faults, int32_t n_faults, void* stream);
 int ftc_protected_conv_finish(ftc_layer* layer, ftc_layer_report* report);
+/* Waits for the clean path of the call in flight and returns its CoC-D screen count
+ * (*flagged > 0: _finish will run the error path, which reads D in NCHW) without ending
+ * the call: a pipeline that skipped the NCHW copy of D (ftc_glue_nchw_optional)
+ * materialises it first. */
+int ftc_protected_conv_peek(ftc_layer* layer, int32_t* flagged);
 /* Abandon the call in flight (a pipeline replays it on repaired input): waits for the
  * clean path to drain and drops its verdict without running the error path. */
 int ftc_protected_conv_cancel(ftc_layer* layer);
@@ -411,6 +416,11 @@ int ftc_glue_act_pool_nhwc(const float* in, float* out, float* out_nhwc, int32_t
 int64_t ftc_glue_ws_doubles(int32_t N, int32_t C, int32_t H, int32_t k, int32_t s, int32_t p);
 int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
                           int32_t act, int32_t k, int32_t s, int32_t p, double* ws, void* stream);
+/* 1 when ftc_glue_act_pool_cd1 accepts out == NULL for this shape: the pass then writes
+ * only the channel-last copy (and Cd1) -- the consumer's clean path reads nothing else,
+ * saving 4 of the 12 bytes per element an activation pass moves.  The NCHW tensor is
+ * needed again only by the consumer's error path (see ftc_protected_conv_peek). */
+int32_t ftc_glue_nchw_optional(const float* in, int32_t C, int32_t H, int32_t k, int32_t s, int32_t p);
 /* out = act(a + b) elementwise over n values (b may be NULL) */
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act,
                      void* stream);

@@ -30,7 +30,8 @@ EXPORTS = (
     "ftc_profile_layer", "ftc_layer_desc", "ftc_glue_ws_doubles", "ftc_glue_act_pool_cd1",
     "ftc_protected_conv_launch_cd1", "ftc_mt64_uniform", "ftc_conv_backward", "ftc_protected_backward",
     "ftc_conv_backward_host", "ftc_protected_backward_host", "ftc_isolated_scheme",
-    "ftc_protected_conv_cancel", "ftc_layer_detect_record",
+    "ftc_protected_conv_cancel", "ftc_layer_detect_record", "ftc_protected_conv_peek",
+    "ftc_glue_nchw_optional",
     "ftc_device_alloc", "ftc_device_free", "ftc_memcpy", "ftc_memset_zero",
 )
 
@@ -167,6 +168,9 @@ def lib():
         L.ftc_glue_ws_doubles.argtypes = [i32] * 6
         L.ftc_glue_ws_doubles.restype = C.c_int64
         L.ftc_glue_act_pool_cd1.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]
+        L.ftc_glue_nchw_optional.argtypes = [vp, i32, i32, i32, i32, i32]
+        L.ftc_glue_nchw_optional.restype = i32
+        L.ftc_protected_conv_peek.argtypes = [vp, C.POINTER(i32)]
         L.ftc_protected_conv_launch_cd1.argtypes = [vp, C.POINTER(Plan), vp, vp, vp, C.POINTER(Fault), i32, vp]
         L.ftc_glue_pad_crop.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp]
         L.ftc_device_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]

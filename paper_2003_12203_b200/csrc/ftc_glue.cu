@@ -604,6 +604,24 @@ int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStrea
   return FTC_OK;
 }
 
+// Which form of k_act_v4_cd1 (if any) takes a glue pass: the 16-byte form, the 2x2 pool
+// form or the scalar-access form; only these run without an NCHW output (out == NULL).
+struct V4Form {
+  bool vec, pool2, any;
+};
+V4Form v4_form(const float* in, const float* out, int C, int H, int k, int s, int p) {
+  static const bool v4_off = getenv("FTC_GLUE_V4") && atoi(getenv("FTC_GLUE_V4")) == 0;
+  const int Ho = (H + 2 * p - k) / s + 1;
+  const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  // the scalar-access form only pays on large planes (AlexNet's 13x13: 80 vs 75 us)
+  V4Form f;
+  f.vec = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0 && aligned;
+  const bool plain = f.vec || (k == 1 && s == 1 && p == 0 && H * H >= 1024);
+  f.pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0 && aligned;
+  f.any = (plain || f.pool2) && C % 32 == 0 && !v4_off;
+  return f;
+}
+
 int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, int C, int H, int act, int k,
                              int s, int p, double* ws, cudaStream_t st) {
   // 8-position x 32-channel tiles looping over image groups: measured faster for the
@@ -614,13 +632,9 @@ int launch_act_pool_nhwc_cd1(const float* in, float* out, float* out_t, int N, i
   const Cd1Ws w = cd1_ws_layout(N, C, Ho, per);
   const int G = act_pool_groups(N, C, Ho);
   const int NG = (N + G - 1) / G;
-  static const bool v4_off = getenv("FTC_GLUE_V4") && atoi(getenv("FTC_GLUE_V4")) == 0;
-  const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  // the scalar-access form only pays on large planes (AlexNet's 13x13: 80 vs 75 us)
-  const bool vec = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0 && aligned;
-  const bool plain = vec || (k == 1 && s == 1 && p == 0 && H * H >= 1024);
-  const bool pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0 && aligned;
-  if ((plain || pool2) && C % 32 == 0 && !v4_off) {
+  const V4Form vf = v4_form(in, out, C, H, k, s, p);
+  const bool vec = vf.vec, pool2 = vf.pool2;
+  if (vf.any) {
     // 32-position tiles: fewer tiles than the 8-position layout the workspace is sized
     // for, and no more image groups than it holds
     const int HW = Ho * Ho;
@@ -746,8 +760,13 @@ int64_t ftc_glue_ws_doubles(int32_t N, int32_t C, int32_t H, int32_t k, int32_t 
 
 int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t N, int32_t C, int32_t H,
                           int32_t act, int32_t k, int32_t s, int32_t p, double* ws, void* stream) {
-  if (k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || !in || !out || (out_nhwc && C % 32)) {
+  if (k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || !in || (!out && !out_nhwc) || (out_nhwc && C % 32)) {
     set_error(FTC_CONFIG_ERROR, "bad pooling window, null buffer or NHWC output with C % 32 != 0");
+    return FTC_CONFIG_ERROR;
+  }
+  // out == NULL: the consumer conv reads only the NHWC copy (ftc_glue_nchw_optional)
+  if (!out && !v4_form(in, nullptr, C, H, k, s, p).any) {
+    set_error(FTC_CONFIG_ERROR, "this glue shape needs its NCHW output (see ftc_glue_nchw_optional)");
     return FTC_CONFIG_ERROR;
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -765,6 +784,11 @@ int ftc_glue_act_pool_cd1(const float* in, float* out, float* out_nhwc, int32_t 
   const int rc = launch_act_pool(in, out, N * C, H, act, k, s, p, Ho, st);
   if (rc != FTC_OK) return rc;
   return launch_cd1_parts(out, N, (long long)C * Ho * Ho, ws, st, C, Ho);
+}
+
+int32_t ftc_glue_nchw_optional(const float* in, int32_t C, int32_t H, int32_t k, int32_t s, int32_t p) {
+  if (k <= 0 || s <= 0 || p < 0 || H + 2 * p < k || !in) return 0;
+  return v4_form(in, nullptr, C, H, k, s, p).any ? 1 : 0;
 }
 
 int ftc_glue_add_act(const float* a, const float* b, float* out, int64_t n, int32_t act, void* stream) {

@@ -1302,6 +1302,14 @@ int ftc_protected_conv_finish(ftc_layer* L, ftc_layer_report* rep) {
   return st;
 }
 
+int ftc_protected_conv_peek(ftc_layer* L, int32_t* flagged) {
+  if (!L || !flagged) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");
+  if (!L->inflight) RET_ERR(FTC_INVALID_ARGUMENT, "no protected call in flight");
+  FTC_CUDA_CHECK(cudaEventSynchronize(L->ev_done));
+  *flagged = ((volatile DetectStats*)L->fstats_h)->flagged;
+  return FTC_OK;
+}
+
 int ftc_protected_check(ftc_layer* L, const ftc_plan* plan, const float* D, float* O,
                         ftc_layer_report* rep, void* stream) {
   if (!L || !plan || !D || !O || !rep) RET_ERR(FTC_INVALID_ARGUMENT, "null argument");

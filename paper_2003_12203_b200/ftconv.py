@@ -357,6 +357,13 @@ class ProtectedConv:
         _check(_abi.lib().ftc_protected_conv_launch_cd1(self.h, C.byref(self._pl), _ptr(D), _ptr(O), _ptr(cd1),
                                                         arr, n, _stream_ptr(stream)), "launch_cd1")
 
+    def peek_flagged(self) -> int:
+        """Wait for the in-flight call's clean path; > 0 when finish() will run the error
+        path (ftc_protected_conv_peek).  The call stays in flight."""
+        n = C.c_int32(0)
+        _check(_abi.lib().ftc_protected_conv_peek(self.h, C.byref(n)), "peek")
+        return int(n.value)
+
     def cancel(self) -> None:
         """Drop the call in flight without judging it (its input was stale)."""
         _check(_abi.lib().ftc_protected_conv_cancel(self.h), "cancel")

@@ -209,9 +209,14 @@ def net_input(net, batch, seed):
 class ProtectedNet:
     """All layers of one net on one device (one data-parallel shard)."""
 
-    def __init__(self, net, batch: int, seed: int, dev, taus=None, rc=True, clc=True):
+    def __init__(self, net, batch: int, seed: int, dev, taus=None, rc=True, clc=True, elide_nchw=False):
         import torch
         self.net, self.batch, self.dev = net, batch, dev
+        # elide_nchw: a glue pass whose output only feeds one conv of the TMA im2col engine
+        # writes just the channel-last copy that conv reads (8 instead of 12 bytes per
+        # element for an activation pass); the NCHW tensor is materialised again only when
+        # the consumer's CoC-D screen fires (its error path reads D in NCHW)
+        self.elide_nchw = elide_nchw
         self.torch = torch
         self.sh, self.convs = shapes(net)
         self.weights = net_weights(net, seed)
@@ -251,12 +256,19 @@ class ProtectedNet:
                 if ptr:
                     self.nhwc_target[op.dst] = (L, ptr)
         self.out_name = net.get("output", "out")
+        self.elidable, self.nchw_valid = {}, {}
+        if elide_nchw:
+            for op in net["ops"]:
+                if isinstance(op, ActPool) and op.dst in self.nhwc_target and op.dst != self.out_name:
+                    c, h = self.sh[op.src]
+                    if _abi.lib().ftc_glue_nchw_optional(self.buf[op.src].data_ptr(), c, h, op.k, op.s, op.p):
+                        self.elidable[op.dst] = op
         self.flops = sum(2.0 * batch * op.M * E * E * Cin * op.R * op.R for op, Cin, H, E in self.convs)
 
     def set_input(self, x):
         self.buf["x"].copy_(x if not isinstance(x, np.ndarray) else self.torch.from_numpy(x))
 
-    def _glue(self, op, stream, protected=True):
+    def _glue(self, op, stream, protected=True, faults=None):
         L = _abi.lib()
         s = stream.cuda_stream
         if isinstance(op, ActPool):
@@ -265,7 +277,12 @@ class ProtectedNet:
             nhwc = None
             if op.dst in self.nhwc_target:
                 Lc, nhwc = self.nhwc_target[op.dst]
-            _check(L.ftc_glue_act_pool_cd1(self.buf[op.src].data_ptr(), self.buf[op.dst].data_ptr(), nhwc,
+            # the consumer's pre-conv faults are applied to the NCHW tensor: keep it then
+            elide = op.dst in self.elidable and not any(
+                f.target != "output" for f in (faults or {}).get(Lc.name, ()))
+            self.nchw_valid[op.dst] = not elide
+            _check(L.ftc_glue_act_pool_cd1(self.buf[op.src].data_ptr(),
+                                           None if elide else self.buf[op.dst].data_ptr(), nhwc,
                                            self.batch, c, h, ACT[op.act], op.k, op.s, op.p,
                                            ws.data_ptr() if (ws is not None and protected) else None, s),
                    "act_pool_cd1")
@@ -289,6 +306,8 @@ class ProtectedNet:
                     L.launch_cd1(self.buf[op.src], self.buf[op.dst], self.ck[op.src], self.plans[op.dst],
                                  (faults or {}).get(op.dst, ()), stream)
                     if sync_each:
+                        if not self.nchw_valid.get(op.src, True) and L.peek_flagged() > 0:
+                            self.materialize(op.src, stream)
                         reps[op.dst] = L.finish()
                 elif protected:
                     L.launch(self.buf[op.src], self.buf[op.dst], self.plans[op.dst],
@@ -298,8 +317,21 @@ class ProtectedNet:
                 else:
                     L.conv_forward(self.buf[op.src], self.buf[op.dst], stream)
             else:
-                self._glue(op, stream, protected)
+                self._glue(op, stream, protected, faults)
         return reps
+
+    def materialize(self, name, stream=None):
+        """Write the NCHW tensor of an elided glue output (same act / pool arithmetic as the
+        channel-last copy, so bitwise the values the conv read)."""
+        if self.nchw_valid.get(name, True):
+            return
+        stream = stream or self.torch.cuda.current_stream()
+        op = self.elidable[name]
+        c, h = self.sh[op.src]
+        _check(_abi.lib().ftc_glue_act_pool_cd1(self.buf[op.src].data_ptr(), self.buf[name].data_ptr(), None,
+                                                self.batch, c, h, ACT[op.act], op.k, op.s, op.p, None,
+                                                stream.cuda_stream), "act_pool (materialize)")
+        self.nchw_valid[name] = True
 
     def launch(self, faults=None, stream=None):
         """Enqueue the clean path of every layer (no host synchronisation)."""
@@ -318,6 +350,8 @@ class ProtectedNet:
             idx += 1
             if not isinstance(op, Conv):
                 continue
+            if not self.nchw_valid.get(op.src, True) and self.layers[op.dst].peek_flagged() > 0:
+                self.materialize(op.src, stream)
             try:
                 rep = self.layers[op.dst].finish()
             except IntegrityError as err:
@@ -622,7 +656,8 @@ class BenchNet:
     inputs are the matching slice of the seeded global input, and its tau_L are
     calibrated on its own shard (shard-local N: SURVEY 8(e))."""
 
-    def __init__(self, name, dev, policy="detection", shard=None, input_seed=1000, calib_seeds=(11, 12)):
+    def __init__(self, name, dev, policy="detection", shard=None, input_seed=1000, calib_seeds=(11, 12),
+                 elide_nchw=False):
         import torch
         net = NETS[name]()
         self.name, self.net, self.dev = name, net, dev
@@ -636,7 +671,7 @@ class BenchNet:
         self.floors_by_policy = {p: detection_floor(self.residuals, t) for p, t in self.taus_by_policy.items()}
         self.policy = policy
         self.taus = self.taus_by_policy[policy]
-        self.pn = ProtectedNet(net, self.batch, 11, dev, self.taus)
+        self.pn = ProtectedNet(net, self.batch, 11, dev, self.taus, elide_nchw=elide_nchw)
         x = np.ascontiguousarray(net_input(net, self.global_batch, input_seed)[lo:hi])
         self.x_host = torch.from_numpy(x).pin_memory()
         self.pn.set_input(self.x_host.to(dev))

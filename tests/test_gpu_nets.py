@@ -218,3 +218,39 @@ def test_yolo_multi_flip_patterns(layer):
         stages.add(got["stage"])
     assert len(stages) >= 2, stages
     pn.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["vgg19", "yolov2"])
+def test_elided_nchw_activations_same_outputs_and_verdicts(name):
+    """elide_nchw: glue passes that feed one TMA im2col conv write the channel-last copy
+    only.  The net's output is bitwise the same, a clean run reports no detection, and a
+    run with one output flip per protected layer (the error path reads D in NCHW, so the
+    pipeline materialises it after peeking at the screen) gives the same verdicts and the
+    same repaired output as the net that keeps every NCHW tensor."""
+    import torch
+    import paper_2003_12203_b200 as F
+    from paper_2003_12203_b200 import nets
+    dev = torch.device("cuda")
+    net = nets.NETS[name]()
+    B = 4
+    x = nets.net_input(net, B, 77)
+    outs, verdicts = [], []
+    for elide in (False, True):
+        pn = nets.ProtectedNet(net, B, 11, dev, elide_nchw=elide)
+        pn.set_input(x)
+        if elide:
+            assert pn.elidable, "no elidable glue outputs"
+        reps = pn.forward()
+        assert not any(r.detected for r in reps.values())
+        clean = pn.output().clone()
+        faults = {op.dst: [F.output_bitflip(1, 2, 3, 3, 29)] for op, *_ in pn.convs}
+        reps = pn.forward(faults)
+        verdicts.append({k: (r.detected, r.stage, tuple(map(tuple, r.corrected_blocks))) for k, r in reps.items()})
+        outs.append((clean.cpu().numpy(), pn.output().cpu().numpy()))
+        if elide:
+            assert any(r.detected for r in reps.values())
+        pn.close()
+    assert verdicts[0] == verdicts[1], (verdicts[0], verdicts[1])
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
