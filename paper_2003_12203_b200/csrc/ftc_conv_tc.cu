@@ -1451,7 +1451,8 @@ bool tc_co5_in_kernel(const TcPlan* p, int N, int E) {
   const long long Kc = (long long)p->K * p->groups;  // Co5 taps run over all channels
   const long long rounds = pos * ((Kc + 32LL * kCkUnroll - 1) / (32LL * kCkUnroll));
   const long long tiles = ((long long)N * E2 + kBM - 1) / kBM * p->ntiles;
-  const long long conv = (tiles + grid - 1) / grid * p->nkc * 1000LL;
+  // ~1,000 cycles per K chunk with the TMA im2col A operand, ~1,800 with the register gather
+  const long long conv = (tiles + grid - 1) / grid * p->nkc * (p->im2col ? 1000LL : 1800LL);
   // a round is two dependent loads (tap entry, then Cd1) through an L2 the conv keeps
   // ~85% busy: measured ~7,300 cycles (VGG-19 c4: the checksum warp finished 0.55 ms after
   // the MMAs, c3 / c2 75-85 us; r02cc ncu lists).  Layers that do not fit take Co5 in the
