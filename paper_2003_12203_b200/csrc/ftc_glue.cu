@@ -147,11 +147,14 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
                                                    float* __restrict__ out_t, int N, int NG, int C, int HW,
                                                    double* __restrict__ ws, long long tick_off, long long slab_off,
                                                    int Ho) {
-  __shared__ float tile[kV4Img][32][33];  // [image][position][channel]
+  // [image][position][channel], rows of 36 floats (16-byte aligned) with the 4-channel
+  // groups of a row XOR-permuted by (position / 8) % 4: the transposing 4-byte writes of a
+  // warp (8 positions 4 apart x 4 channels) and the 16-byte row reads are conflict-free
+  __shared__ __align__(16) float tile[kV4Img][32][36];
   const int tid = threadIdx.x;
   const int cl = tid >> 3, p4 = (tid & 7) * 4;  // load role: channel row, 4 positions
   const int c = blockIdx.y * 32 + cl, pos = blockIdx.x * 32 + p4;
-  const int wc = tid & 31, wp = tid >> 5;     // store role: lane = channel, warp = position row
+  const int g4 = tid & 7, prow = tid >> 3;    // store role: 4-channel group (physical), position row
   const int g = blockIdx.z, G = gridDim.z;
   const int n_lo = g * NG, n_hi = min(N, n_lo + NG);
   // VEC: HW % 4 == 0 and 16-byte aligned tensors, so a thread's 4 positions are one
@@ -254,17 +257,28 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
     }
     if (out_t) {
 #pragma unroll
+      // a thread's 4 positions p4 .. p4+3 share (position / 8), hence one column
+      const int wcol = (((cl >> 2) ^ ((p4 >> 3) & 3)) << 2) | (cl & 3);
+#pragma unroll
       for (int u = 0; u < kV4Img; ++u) {
-        tile[u][p4 + 0][cl] = v[u].x;
-        tile[u][p4 + 1][cl] = v[u].y;
-        tile[u][p4 + 2][cl] = v[u].z;
-        tile[u][p4 + 3][cl] = v[u].w;
+        tile[u][p4 + 0][wcol] = v[u].x;
+        tile[u][p4 + 1][wcol] = v[u].y;
+        tile[u][p4 + 2][wcol] = v[u].z;
+        tile[u][p4 + 3][wcol] = v[u].w;
       }
       __syncthreads();
-      // kV4Img images x 32 positions of 32-channel NHWC rows; warp wp stores rows wp, wp+8, ...
-      for (int row = wp; row < cnt * 32; row += 8) {
-        const int u = row >> 5, pl = row & 31, sp = blockIdx.x * 32 + pl;
-        if (sp < HW) out_t[((long long)(n + u) * HW + sp) * C + blockIdx.y * 32 + wc] = tile[u][pl][wc];
+      // kV4Img images x 32 positions of 32-channel NHWC rows as 16-byte stores: a thread
+      // owns (position row, 4-channel group) of every image, a warp 4 whole rows
+      {
+        const int sp = blockIdx.x * 32 + prow;
+        const int lg = g4 ^ ((prow >> 3) & 3);  // logical group of physical group g4
+        if (sp < HW) {
+          float4* dst = reinterpret_cast<float4*>(out_t + ((long long)n * HW + sp) * C + blockIdx.y * 32 + 4 * lg);
+          const long long istep = (long long)HW * C / 4;
+#pragma unroll
+          for (int u = 0; u < kV4Img; ++u)
+            if (u < cnt) dst[u * istep] = *reinterpret_cast<const float4*>(&tile[u][prow][4 * g4]);
+        }
       }
       __syncthreads();
     }
