@@ -184,8 +184,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Critical-path waits (producers, MMA issuers).  FTC_SPIN_NS > 0 backs off between failed
+// polls: when the pipeline stalls at a tile boundary ten warps spin here at once and
+// take issue slots from the epilogue warps that everyone is waiting for.
+#ifndef FTC_SPIN_NS
+#define FTC_SPIN_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+    if (FTC_SPIN_NS > 0) __nanosleep(FTC_SPIN_NS);
   }
 }
 // off the MMA-critical path (epilogue, B loader): back off between polls so the spinning
@@ -288,6 +295,7 @@ __device__ __forceinline__ void gdone_wait(uint32_t gdone0, uint32_t j, bool laz
     while (!mbar_try_wait(bar, ph)) __nanosleep(64);
   } else {
     while (!mbar_try_wait(bar, ph)) {
+      if (FTC_SPIN_NS > 0) __nanosleep(FTC_SPIN_NS);
     }
   }
 }
@@ -944,9 +952,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
         // per output were a third of a 1-chunk tile's epilogue, VGG c1)
         const int sums = a.rowsum ? 2 : (FUSE ? 1 : 0);
         if (valid) {
+          // running output pointer (one 64-bit add per column; the opaque asm keeps the
+          // compiler from re-deriving op + jj * E2 for every store: that form, with the base
+          // re-read from the constant bank, made the plain tile end ~10 instructions per
+          // output and 3.3K cycles per tile -- SASS + r02cz no-store experiment)
+          float* oq = op;
           if (sums == 0) {
 #pragma unroll
-            for (int jj = 0; jj < HALF; ++jj) op[jj * E2] = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
+            for (int jj = 0; jj < HALF; ++jj) {
+              *oq = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
+              oq += E2;
+              asm volatile("" : "+l"(oq));
+            }
           } else if (sums == 1) {
             // So5 row sum as an error-free FP32 accumulation (TwoSum: s1 + e1 carries the
             // sum to ~2^-46 of the terms' magnitude; the screen's guard band is 1e-3 of
@@ -957,7 +974,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_tc(TcArgs a, const __grid_
 #pragma unroll
             for (int jj = 0; jj < HALF; ++jj) {
               const float val = (float)sum[jj] + (bp ? __ldg(bp + jj) : 0.f);
-              op[jj * E2] = val;
+              *oq = val;
+              oq += E2;
+              asm volatile("" : "+l"(oq));
               const float t = __fadd_rn(s1, val);
               const float bb = __fsub_rn(t, s1);
               e1 = __fadd_rn(e1, __fadd_rn(__fsub_rn(s1, __fsub_rn(t, bb)), __fsub_rn(val, bb)));
