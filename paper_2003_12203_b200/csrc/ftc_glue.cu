@@ -139,7 +139,17 @@ __global__ void __launch_bounds__(256) k_cd1_parts(const float* __restrict__ D, 
 // barrier pair per four images.
 // POOL2: 2x2 stride-2 max-pool after the activation (Ho % 4 == 0, so a thread's 4
 // output positions share a row and read two rows of 8 inputs: four 16-byte loads).
-constexpr int kV4Img = 4;
+#ifndef FTC_V4_PLAIN_IMG
+#define FTC_V4_PLAIN_IMG 8
+#endif
+constexpr int kV4ImgPlain = FTC_V4_PLAIN_IMG;
+// images in flight per thread: 8 for the activation-only form (one 16-byte load per image;
+// VGG-19 ReLU passes 992 / 957 / 944 us per step at 4 / 2 / 8), 2 for the 2x2-pool form
+// (four loads per image: 420 -> 317 us, 4.0 -> 5.3 TB/s; 432 at 1, 408 at 8 -- fewer
+// registers, more resident blocks, shorter load / transpose / store phases per barrier)
+#ifndef FTC_V4_POOL_IMG
+#define FTC_V4_POOL_IMG 2
+#endif
 // CD1 = false: the same pass without the checksum (the unprotected net's glue, so that the
 // ABFT overhead is measured against equally tuned kernels).
 template <int ACT, bool POOL2, bool VEC = true, bool CD1 = true>
@@ -150,6 +160,7 @@ __global__ void __launch_bounds__(256) k_act_v4_cd1(const float* __restrict__ in
   // [image][position][channel], rows of 36 floats (16-byte aligned) with the 4-channel
   // groups of a row XOR-permuted by (position / 8) % 4: the transposing 4-byte writes of a
   // warp (8 positions 4 apart x 4 channels) and the 16-byte row reads are conflict-free
+  constexpr int kV4Img = POOL2 ? FTC_V4_POOL_IMG : kV4ImgPlain;
   __shared__ __align__(16) float tile[kV4Img][32][36];
   const int tid = threadIdx.x;
   const int cl = tid >> 3, p4 = (tid & 7) * 4;  // load role: channel row, 4 positions
