@@ -327,7 +327,11 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
                                                        float* __restrict__ out_t, int N, int NG, int C, int H,
                                                        int kr, int s, int p, int Ho, double* __restrict__ ws,
                                                        long long tick_off, long long slab_off) {
-  __shared__ float tile[2][8][33];
+  // images' windows in flight per thread: 1 for 3x3 windows (9 loads each; AlexNet pools
+  // 152 -> 136 us, ResNet-18 stem pool 477 -> 414 at 2 -> 1), 4 for activation-only passes
+  // of odd planes (351 -> 327 us over ResNet-18's five), 2 otherwise
+  constexpr int IMG = KT == 1 ? 4 : (KT == 3 ? 1 : 2);
+  __shared__ float tile[IMG][8][33];
   const int k = KT > 0 ? KT : kr;
   const int plane = Ho * Ho;
   const int tid = threadIdx.x;
@@ -379,7 +383,6 @@ __global__ void __launch_bounds__(256) k_act_pool_t_cd1(const float* __restrict_
   };
   // IMG images' windows in flight per thread (8 for k = 1 measured slower: VGG-19 relu
   // glue 2.55 vs 2.21 ms per step)
-  constexpr int IMG = 2;
   double acc = 0.0;
   for (int n = n_lo; n < n_hi; n += IMG) {
     const int cnt = min(IMG, n_hi - n);
