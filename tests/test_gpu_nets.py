@@ -44,6 +44,7 @@ def test_net_per_layer_parity_and_clean_verdicts(name, batch):
     torch.cuda.synchronize()
     assert not any(r.detected for r in reps.values()), {k: r.stage for k, r in reps.items() if r.detected}
     worst = 0.0
+    relaxed = []  # layers judged by "at least as close to the FP64 conv as the reference"
     for op, Cin, H, E in pn.convs:
         D = pn.buf[op.src].cpu().numpy()
         Og = pn.buf[op.dst].cpu().numpy()
@@ -57,6 +58,9 @@ def test_net_per_layer_parity_and_clean_verdicts(name, batch):
                              None if b is None else b.astype(np.float64))
             e_gpu, e_ref = close_frac(Og, O64).max(), close_frac(Oo, O64).max()
             assert e_gpu <= e_ref, (op.dst, err, e_gpu, e_ref)
+            relaxed.append((op.dst, float(err), float(e_gpu), float(e_ref)))
+    print(f"{name}: worst |gpu - ref| {worst:.2e}; {len(relaxed)} of {len(pn.convs)} layers needed the FP64 gate "
+          f"(layer, |gpu-ref|, |gpu-f64|, |ref-f64|): {relaxed}")
     pn.close()
 
 
