@@ -767,7 +767,8 @@ class BenchNet:
         if not hasattr(self, "pipe"):
             # a second set of layer handles and activations (same weights and plans) so
             # batch k+1 is enqueued while batch k's verdicts are read
-            self.pn2 = ProtectedNet(self.net, self.batch, 11, self.pn.dev, self.taus)
+            self.pn2 = ProtectedNet(self.net, self.batch, 11, self.pn.dev, self.taus,
+                                    elide_nchw=self.pn.elide_nchw)
             self.pipe = HostPipeline([self.pn, self.pn2])
             self.outs_host = [self.out_host, self.pn.torch.empty_like(self.out_host).pin_memory()]
         reps = self.pipe.run([self.x_host] * steps, [self.outs_host[k % 2] for k in range(steps)],
