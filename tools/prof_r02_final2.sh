@@ -17,7 +17,7 @@ F="--set full --clock-control none --import-source on --nvtx --nvtx-include time
 # at most 64 MiB of gpurun_out/; the config-1 report (3 kernels) is kept whole
 R=/tmp/ncurep; mkdir -p $R
 full() {  # name, kernel regex, count, workload
-  timeout 1500 ncu $F -k regex:"$2" -c $3 -o $R/$1 python bench.py --workload $4 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_$1.log 2>&1
+  timeout 1500 ncu $F -f -k regex:"$2" -c $3 -o $R/$1 python bench.py --workload $4 --steps 1 --warmup 3 --no-cpu-baseline --no-extras --campaign-runs 0 > gpurun_out/${PFX}_ncuf_$1.log 2>&1
   ncu -i $R/$1.ncu-rep --page raw --csv > gpurun_out/${PFX}_$1_raw.csv 2>/dev/null
 }
 full vgg_convs k_conv_tc 16 vgg19
