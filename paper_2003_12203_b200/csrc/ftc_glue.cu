@@ -634,6 +634,9 @@ int launch_cd1_parts(const float* D, int N, long long per, double* ws, cudaStrea
 
 // Which form of k_act_v4_cd1 (if any) takes a glue pass: the 16-byte form, the 2x2 pool
 // form or the scalar-access form; only these run without an NCHW output (out == NULL).
+#ifndef FTC_V4_SCALAR_MIN
+#define FTC_V4_SCALAR_MIN 64
+#endif
 struct V4Form {
   bool vec, pool2, any;
 };
@@ -641,10 +644,12 @@ V4Form v4_form(const float* in, const float* out, int C, int H, int k, int s, in
   static const bool v4_off = getenv("FTC_GLUE_V4") && atoi(getenv("FTC_GLUE_V4")) == 0;
   const int Ho = (H + 2 * p - k) / s + 1;
   const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (!out || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  // the scalar-access form only pays on large planes (AlexNet's 13x13: 80 vs 75 us)
+  // the scalar-access form for odd planes down to 8x8 (with the 16-byte channel-last stores it
+  // wins on AlexNet's 13x13 and ResNet-18's 29x29 / 15x15 too: 82.6K -> 83.5K, 33.2K -> 33.7K
+  // images/s; before them it lost on 13x13, 80 vs 75 us)
   V4Form f;
   f.vec = k == 1 && s == 1 && p == 0 && (H * H) % 4 == 0 && aligned;
-  const bool plain = f.vec || (k == 1 && s == 1 && p == 0 && H * H >= 1024);
+  const bool plain = f.vec || (k == 1 && s == 1 && p == 0 && H * H >= FTC_V4_SCALAR_MIN);
   f.pool2 = k == 2 && s == 2 && p == 0 && H % 2 == 0 && Ho % 4 == 0 && aligned;
   f.any = (plain || f.pool2) && C % 32 == 0 && !v4_off;
   return f;
