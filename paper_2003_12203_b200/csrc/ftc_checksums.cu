@@ -334,18 +334,18 @@ __global__ void __launch_bounds__(32 * kSeqWarps) k_seq_sums567(VirtualO v, int 
 
 // So5/So6/So7, staged form: a block owns 32 positions.  Warp 0 is the chain warp, a lane
 // per position running its three chains (s5, s6, s7: three independent DADDs per term, so
-// the add latency is covered and the FP64 issue rate sets the pace); warps 1-7 stage the
+// the add latency is covered); the 12 warps on the other three sub-partitions stage the
 // terms ahead of it: coalesced loads of O (lane = position), the verifier's FP64
 // overrides, the exact products m*x and n*x, written as FP64 rows [family][term][32
-// positions] into a double-buffered shared-memory tile.  The loaders hold the tile after
-// next in registers, so a load has a whole chain tile (~1.2K cycles) to land.  Same
+// positions] into a double-buffered shared-memory tile.  The loaders hold the next two
+// tiles in registers, so a load has two chain tiles (~3K cycles each) to land.  Same
 // operations in the same order as k_seq_sums567 (n outer, m inner; x, m*x, n*x exact
 // products, one DADD each), hence bitwise the same sums, at ~23 cycles per term instead
 // of ~50 (one chain per warp fed by shuffles): AlexNet conv2 So5-7 877 -> 393 us.
 constexpr int kStT = 128;        // terms per staged tile
-constexpr int kStLW = 12;            // loader warps: warps 1-15 of the block except 4, 8, 12 -- the chain warp's
-                                     // scheduler (sub-partition 0) issues for nobody else (with loaders beside it the
-                                     // chain warp got every fourth issue slot: ~32 cycles per term)
+constexpr int kStLW = 12;            // loader warps: warps 1-15 of the block except 4, 8, 12, so the chain warp's
+                                     // scheduler (sub-partition 0) issues for nobody else (7, 15 and 12 loader warps
+                                     // measured alike: the chain warp's load -> add order set the pace)
 constexpr int kStLoad = kStLW * 32;  // loader threads
 constexpr int kStPer = (kStT * 32 + kStLoad - 1) / kStLoad;  // elements per loader thread and tile
 template <bool VIRT>
