@@ -225,7 +225,7 @@ def test_yolo_multi_flip_patterns(layer):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["vgg19", "yolov2"])
+@pytest.mark.parametrize("name", ["vgg19", "yolov2", "alexnet", "resnet18"])
 def test_elided_nchw_activations_same_outputs_and_verdicts(name):
     """elide_nchw: glue passes that feed one TMA im2col conv write the channel-last copy
     only.  The net's output is bitwise the same, a clean run reports no detection, and a
